@@ -1,0 +1,182 @@
+// a11: CIC-PIC deposit and gather+push (reading R14);
+// a12: parareal correction + stopping norms (eq. parareal_correction P:154-161,
+// eq. stop_criteria); the test-only push and a finiteness check.
+#include "pif_internal.cuh"
+
+namespace pif {
+
+__device__ __forceinline__ void cic_1d(double x, double inv_h, int Ng, int& i0, int& i1,
+                                       double& w0, double& w1) {
+  double s = x * inv_h;
+  double fi = floor(s);
+  double f = s - fi;
+  int i = (int)fi;
+  i0 = ((i % Ng) + Ng) % Ng;
+  i1 = i0 + 1 == Ng ? 0 : i0 + 1;
+  w0 = 1.0 - f;
+  w1 = f;
+}
+
+// rho_p += W_pj (the q / h^3 factor is applied in the Poisson kernel).
+__global__ void k_cic_deposit(const double* __restrict__ x, int64_t stride, int64_t n, int Ng,
+                              double inv_h, double* __restrict__ grid) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int i0[3], i1[3];
+  double w0[3], w1[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cic_1d(x[d * stride + j], inv_h, Ng, i0[d], i1[d], w0[d], w1[d]);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int ix = (c & 4) ? i1[0] : i0[0];
+    int iy = (c & 2) ? i1[1] : i0[1];
+    int iz = (c & 1) ? i1[2] : i0[2];
+    double wt = ((c & 4) ? w1[0] : w0[0]) * ((c & 2) ? w1[1] : w0[1]) * ((c & 1) ? w1[2] : w0[2]);
+    atomicAdd(grid + ((int64_t)ix * Ng + iy) * Ng + iz, wt);
+  }
+}
+
+__global__ void k_cic_gather_push(const double* __restrict__ g3, double* __restrict__ x,
+                                  double* __restrict__ v, int64_t stride, int64_t n, int Ng,
+                                  double inv_h, PushArgs P) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t n3 = (int64_t)Ng * Ng * Ng;
+  double x0 = x[j], x1 = x[stride + j], x2 = x[2 * stride + j];
+  int i0[3], i1[3];
+  double w0[3], w1[3];
+  cic_1d(x0, inv_h, Ng, i0[0], i1[0], w0[0], w1[0]);
+  cic_1d(x1, inv_h, Ng, i0[1], i1[1], w0[1], w1[1]);
+  cic_1d(x2, inv_h, Ng, i0[2], i1[2], w0[2], w1[2]);
+  double E0 = 0, E1 = 0, E2 = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int ix = (c & 4) ? i1[0] : i0[0];
+    int iy = (c & 2) ? i1[1] : i0[1];
+    int iz = (c & 1) ? i1[2] : i0[2];
+    double wt = ((c & 4) ? w1[0] : w0[0]) * ((c & 2) ? w1[1] : w0[1]) * ((c & 1) ? w1[2] : w0[2]);
+    int64_t idx = ((int64_t)ix * Ng + iy) * Ng + iz;
+    E0 += wt * g3[idx];
+    E1 += wt * g3[n3 + idx];
+    E2 += wt * g3[2 * n3 + idx];
+  }
+  double v0 = v[j], v1 = v[stride + j], v2 = v[2 * stride + j];
+  push_particle(x0, x1, x2, v0, v1, v2, E0, E1, E2, P);
+  x[j] = x0;
+  x[stride + j] = x1;
+  x[2 * stride + j] = x2;
+  v[j] = v0;
+  v[stride + j] = v1;
+  v[2 * stride + j] = v2;
+}
+
+__global__ void k_push_only(double* __restrict__ x, double* __restrict__ v,
+                            const double* __restrict__ E, int64_t stride, int64_t n, PushArgs P) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double x0 = x[j], x1 = x[stride + j], x2 = x[2 * stride + j];
+  double v0 = v[j], v1 = v[stride + j], v2 = v[2 * stride + j];
+  push_particle(x0, x1, x2, v0, v1, v2, E[j], E[stride + j], E[2 * stride + j], P);
+  x[j] = x0;
+  x[stride + j] = x1;
+  x[2 * stride + j] = x2;
+  v[j] = v0;
+  v[stride + j] = v1;
+  v[2 * stride + j] = v2;
+}
+
+// Canonical states: [x0..|x1..|x2..|v0..|v1..|v2..], 6n doubles.
+// U = F + Gn - Go (x wrapped, R17); partial sums of
+// {|mi(Gn.x - Go.x)|^2, |Gn.x|^2, |Gn.v - Go.v|^2, |Gn.v|^2} (eq. stop_criteria).
+__device__ __forceinline__ void block_sum4_m(double a[4], double* __restrict__ dst) {
+  __shared__ double sh[4][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sh[q][wid] = a[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) {
+      double s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[q][w];
+      dst[q] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_correct_norms(const double* __restrict__ F,
+                                                       const double* __restrict__ Gn,
+                                                       const double* __restrict__ Go,
+                                                       double* __restrict__ U, int64_t n, double L,
+                                                       double* __restrict__ partials) {
+  double a[4] = {0, 0, 0, 0};
+  const int64_t tot = 3 * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // positions
+    double gn = Gn[i], go = Go[i];
+    double ux = (F[i] + gn) - go;
+    if (U) U[i] = wrapL(ux, L);
+    double d = gn - go;
+    d = d - L * rint(d / L);
+    a[0] += d * d;
+    a[1] += gn * gn;
+    // velocities
+    double hn = Gn[tot + i], ho = Go[tot + i];
+    if (U) U[tot + i] = (F[tot + i] + hn) - ho;
+    double e = hn - ho;
+    a[2] += e * e;
+    a[3] += hn * hn;
+  }
+  block_sum4_m(a, partials + 4 * blockIdx.x);
+}
+
+__global__ void __launch_bounds__(256) k_reduce4(const double* __restrict__ partials, int nparts,
+                                                 double* __restrict__ out4) {
+  double a[4] = {0, 0, 0, 0};
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] += partials[4 * i + q];
+  block_sum4_m(a, out4);
+}
+
+__global__ void k_check_finite(const double* __restrict__ a, int64_t count, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(a[i])) atomicExch(flag, 1);
+}
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_cic_deposit(const double* x, int64_t stride, int64_t n, int Ng, double inv_h,
+                               double* grid, cudaStream_t st) {
+  if (n > 0) k_cic_deposit<<<nblk(n, 256), 256, 0, st>>>(x, stride, n, Ng, inv_h, grid);
+  return cudaGetLastError();
+}
+cudaError_t launch_cic_gather_push(const double* grid3, double* x, double* v, int64_t stride,
+                                   int64_t n, int Ng, double inv_h, const PushArgs& P,
+                                   cudaStream_t st) {
+  if (n > 0) k_cic_gather_push<<<nblk(n, 256), 256, 0, st>>>(grid3, x, v, stride, n, Ng, inv_h, P);
+  return cudaGetLastError();
+}
+cudaError_t launch_push_only(double* x, double* v, const double* E, int64_t stride, int64_t n,
+                             const PushArgs& P, cudaStream_t st) {
+  if (n > 0) k_push_only<<<nblk(n, 256), 256, 0, st>>>(x, v, E, stride, n, P);
+  return cudaGetLastError();
+}
+cudaError_t launch_correct_norms(const double* F, const double* Gn, const double* Go, double* U,
+                                 int64_t n, double L, double* partials, double* out4,
+                                 cudaStream_t st) {
+  k_correct_norms<<<kReduceBlocks, 256, 0, st>>>(F, Gn, Go, U, n, L, partials);
+  k_reduce4<<<1, 256, 0, st>>>(partials, kReduceBlocks, out4);
+  return cudaGetLastError();
+}
+cudaError_t launch_check_finite(const double* a, int64_t count, int* flag, cudaStream_t st) {
+  k_check_finite<<<kReduceBlocks, 256, 0, st>>>(a, count, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace pif

@@ -1,0 +1,1026 @@
+// C ABI of the PIF library (include/pif.h): context, NUFFT plans, workspace,
+// the step loop (a0..a8 of SURVEY.md Sec. 8a), diagnostics, parareal driver
+// (fine/coarse propagation, correction, NCCL hand-off) and test-only exports.
+#include <math.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "pif_internal.cuh"
+
+using namespace pif;
+
+namespace {
+
+thread_local std::string g_err;
+
+pif_status fail(pif_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(PIF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+#define CUFFT(call)                                                                       \
+  do {                                                                                    \
+    cufftResult r_ = (call);                                                              \
+    if (r_ != CUFFT_SUCCESS)                                                              \
+      return fail(PIF_ERR_CUDA, std::string(#call) + ": cufft error " + std::to_string((int)r_)); \
+  } while (0)
+#define NC(call)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(PIF_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+#define TRY(call)                 \
+  do {                            \
+    pif_status s_ = (call);       \
+    if (s_ != PIF_OK) return s_;  \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// NUFFT parameters (reading R12): w = ceil(-log10(eps/10)), beta = c(w) w, n =
+// smallest power of two >= max(2N, 2w); ES kernel and its Fourier transform
+// psi^(xi) = int psi(t) cos(xi t) dt by Gauss-Legendre quadrature.
+// ---------------------------------------------------------------------------
+int es_width(double tol) {
+  int w = (int)std::ceil(-std::log10(tol / 10.0) - 1e-9);
+  return std::min(16, std::max(2, w));
+}
+double es_beta(int w) {
+  double c = w == 2 ? 2.20 : w == 3 ? 2.26 : w == 4 ? 2.38 : 2.30;
+  return c * w;
+}
+double es_host(double t, double w, double beta) {
+  double z = 2.0 * t / w;
+  double r = 1.0 - z * z;
+  return r >= 0.0 ? std::exp(beta * (std::sqrt(r) - 1.0)) : 0.0;
+}
+void gauss_legendre(int q, std::vector<double>& x, std::vector<double>& wt) {
+  x.resize(q);
+  wt.resize(q);
+  for (int i = 0; i < q; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (q + 0.5)), dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= q; ++k) {
+        double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = q * (z * p1 - p0) / (z * z - 1.0);
+      double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= q; ++k) {
+        double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = q * (z * p1 - p0) / (z * z - 1.0);
+    }
+    x[i] = z;
+    wt[i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+double es_hat(double xi, int w, double beta) {
+  static thread_local std::vector<double> gx, gw;
+  if (gx.empty()) gauss_legendre(200, gx, gw);
+  double half = 0.5 * w, s = 0.0;
+  for (size_t i = 0; i < gx.size(); ++i) {
+    double t = 0.5 * half * (gx[i] + 1.0);  // [0, w/2]
+    s += gw[i] * es_host(t, w, beta) * std::cos(xi * t);
+  }
+  return 2.0 * 0.5 * half * s;  // even integrand: 2 * int_0^{w/2}
+}
+
+enum { PH_SORT = 0, PH_SPREAD, PH_FFT_FWD, PH_BOX, PH_ALLREDUCE, PH_POISSON, PH_FFT_INV,
+       PH_INTERP_PUSH, PH_PIC_DEPOSIT, PH_PIC_GATHER_PUSH, PH_OTHER, PH_COUNT };
+static_assert(PH_COUNT == PIF_NPHASES, "phase count");
+
+struct Plan {
+  bool valid = false;
+  int kind = 0, N = 0, order = 1;
+  double tol = 0, dt = 0;
+  Brick g{};
+  int64_t nbricks = 0;
+  int n = 0;  // FFT grid points per dim (PIF: upsampled n; PIC: Ng)
+  double* grid = nullptr;
+  double2* spec = nullptr;
+  double2* G3 = nullptr;
+  double* grid3 = nullptr;
+  double2* box = nullptr;
+  double* cor = nullptr;  // 1/psi^(2 pi m / n), m in [-N/2, N/2]
+  double* S = nullptr;    // S(k_m), m in [-N/2, N/2]
+  std::vector<double> hcor, hS;
+  cufftHandle fwd = 0, inv = 0;
+  size_t wfwd = 0, winv = 0;
+  int64_t box_elems() const { return (int64_t)(N + 1) * (N + 1) * (N / 2 + 1); }
+  int64_t grid_pts() const { return (int64_t)n * n * n; }
+  int64_t spec_elems() const { return (int64_t)n * n * (n / 2 + 1); }
+};
+
+}  // namespace
+
+struct pif_ctx_s {
+  Phys ph{};
+  Plan plan[2];
+  int64_t Nglob = 0, first = 0, nloc = 0;
+  double q = 0, m = 0;
+  int device = 0, rank = 0, world = 1, space_size = 1, time_size = 1, s_idx = 0, t_idx = 0;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm_world = nullptr, comm_space = nullptr, comm_time = nullptr;
+  // workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  double *xA = nullptr, *vA = nullptr, *xB = nullptr, *vB = nullptr;
+  int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *counts = nullptr,
+      *offsets = nullptr, *flag = nullptr;
+  double *partials = nullptr, *red = nullptr;
+  void* fft_work = nullptr;
+  int64_t max_bins = 1;
+  // time level
+  bool has_state = false, pending = false, box_fresh = false;
+  int pending_plan = 0;
+  double* host_red = nullptr;  // pinned 8 doubles
+  // phase profiling (pif_profile): event pairs per phase, launch counter
+  bool prof = false;
+  std::vector<cudaEvent_t> ev[PIF_NPHASES];
+  size_t ev_used[PIF_NPHASES] = {};
+  int64_t launches = 0;
+};
+
+namespace {
+
+// Walk the workspace layout (256-byte aligned buffers); base == nullptr: size only.
+size_t layout(pif_ctx c, char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    off = (off + 255) & ~(size_t)255;
+    char* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  };
+  const int64_t n = std::max<int64_t>(c->nloc, 1);
+  c->xA = (double*)take(3 * n * sizeof(double));
+  c->vA = (double*)take(3 * n * sizeof(double));
+  c->xB = (double*)take(3 * n * sizeof(double));
+  c->vB = (double*)take(3 * n * sizeof(double));
+  c->idA = (int*)take(n * sizeof(int));
+  c->idB = (int*)take(n * sizeof(int));
+  c->key = (int*)take(n * sizeof(int));
+  c->rnk = (int*)take(n * sizeof(int));
+  c->counts = (int*)take(c->max_bins * sizeof(int));
+  c->offsets = (int*)take((c->max_bins + 1) * sizeof(int));
+  c->flag = (int*)take(64);
+  c->partials = (double*)take(4 * kReduceBlocks * sizeof(double));
+  c->red = (double*)take(16 * sizeof(double));
+  size_t fw = 0;
+  for (int i = 0; i < 2; ++i) {
+    Plan& p = c->plan[i];
+    if (!p.valid) continue;
+    fw = std::max(fw, std::max(p.wfwd, p.winv));
+    p.grid = (double*)take(p.grid_pts() * sizeof(double));
+    p.spec = (double2*)take(p.spec_elems() * sizeof(double2));
+    p.G3 = (double2*)take(3 * p.spec_elems() * sizeof(double2));
+    p.grid3 = (double*)take(3 * p.grid_pts() * sizeof(double));
+    if (p.kind == PIF_PROP_PIF_NUFFT) {
+      p.box = (double2*)take(p.box_elems() * sizeof(double2));
+      p.cor = (double*)take((p.N + 1) * sizeof(double));
+      p.S = (double*)take((p.N + 1) * sizeof(double));
+    }
+  }
+  c->fft_work = take(std::max<size_t>(fw, 256));
+  return off + 256;
+}
+
+pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
+  Plan& p = c->plan[which];
+  if (pr->dt <= 0 || !std::isfinite(pr->dt)) return fail(PIF_ERR_ARG, "dt must be > 0");
+  if (pr->spline_order < 1) return fail(PIF_ERR_ARG, "spline_order must be >= 1");
+  p.kind = pr->kind;
+  p.N = pr->n;
+  p.order = pr->spline_order;
+  p.tol = pr->tol;
+  p.dt = pr->dt;
+  const double L = c->ph.L;
+  if (pr->kind == PIF_PROP_PIF_NUFFT) {
+    if (pr->n < 2 || pr->n % 2 || pr->n > 256) return fail(PIF_ERR_ARG, "PIF n must be even in [2, 256]");
+    if (!(pr->tol >= 1e-15 && pr->tol < 1e-1)) return fail(PIF_ERR_ARG, "tol must be in [1e-15, 1e-1)");
+    int w = es_width(pr->tol);
+    int n = 2;
+    while (n < std::max(2 * pr->n, 2 * w)) n *= 2;
+    int R = (w + 3 <= 8) ? 8 : (w + 3 <= 12) ? 12 : 16;
+    Brick& g = p.g;
+    g.n = n;
+    g.w = w;
+    g.hw = (w - 1) / 2;
+    g.odd = w & 1;
+    g.R = R;
+    g.b = R - w + 1;
+    g.nb = (n + g.b - 1) / g.b;
+    g.scale = n / L;
+    g.beta = es_beta(w);
+    p.n = n;
+    p.nbricks = (int64_t)g.nb * g.nb * g.nb;
+    c->max_bins = std::max(c->max_bins, p.nbricks);
+    const int H = p.N / 2;
+    p.hcor.resize(p.N + 1);
+    p.hS.resize(p.N + 1);
+    const double h = L / p.N;
+    for (int m = -H; m <= H; ++m) {
+      p.hcor[m + H] = 1.0 / es_hat(2.0 * M_PI * m / n, w, g.beta);
+      double k = 2.0 * M_PI * m / L, u = 0.5 * k * h;
+      double sinc = m == 0 ? 1.0 : std::sin(u) / u;
+      p.hS[m + H] = std::pow(sinc, p.order + 1);  // S(k) = sinc^(m+1)(k h / 2), R3/R4
+    }
+  } else if (pr->kind == PIF_PROP_PIC_CIC) {
+    if (pr->n < 4 || pr->n % 2 || pr->n > 512) return fail(PIF_ERR_ARG, "PIC n must be even in [4, 512]");
+    if (pr->spline_order != 1) return fail(PIF_ERR_ARG, "PIC supports spline_order 1 (CIC) only");
+    p.n = pr->n;
+  } else {
+    return fail(PIF_ERR_ARG, "unknown propagator kind");
+  }
+  const int n = p.n;
+  CUFFT(cufftCreate(&p.fwd));
+  CUFFT(cufftSetAutoAllocation(p.fwd, 0));
+  CUFFT(cufftMakePlan3d(p.fwd, n, n, n, CUFFT_D2Z, &p.wfwd));
+  CUFFT(cufftCreate(&p.inv));
+  CUFFT(cufftSetAutoAllocation(p.inv, 0));
+  int dims[3] = {n, n, n};
+  CUFFT(cufftMakePlanMany(p.inv, 3, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 3, &p.winv));
+  CUFFT(cufftSetStream(p.fwd, c->st));
+  CUFFT(cufftSetStream(p.inv, c->st));
+  p.valid = true;
+  return PIF_OK;
+}
+
+// Host-only argument validation (no CUDA calls), so bad input fails fast.
+pif_status validate_prop(const pif_propagator* pr) {
+  if (!(pr->dt > 0) || !std::isfinite(pr->dt)) return fail(PIF_ERR_ARG, "dt must be > 0");
+  if (pr->spline_order < 1) return fail(PIF_ERR_ARG, "spline_order must be >= 1");
+  if (pr->kind == PIF_PROP_PIF_NUFFT) {
+    if (pr->n < 2 || pr->n % 2 || pr->n > 256) return fail(PIF_ERR_ARG, "PIF n must be even in [2, 256]");
+    if (!(pr->tol >= 1e-15 && pr->tol < 1e-1)) return fail(PIF_ERR_ARG, "tol must be in [1e-15, 1e-1)");
+  } else if (pr->kind == PIF_PROP_PIC_CIC) {
+    if (pr->n < 4 || pr->n % 2 || pr->n > 512) return fail(PIF_ERR_ARG, "PIC n must be even in [4, 512]");
+    if (pr->spline_order != 1) return fail(PIF_ERR_ARG, "PIC supports spline_order 1 (CIC) only");
+  } else {
+    return fail(PIF_ERR_ARG, "unknown propagator kind");
+  }
+  return PIF_OK;
+}
+
+PushArgs push_args(pif_ctx c, const Plan& p, int kicks, int drift) {
+  PushArgs P{};
+  P.L = c->ph.L;
+  P.dt = p.dt;
+  P.h = 0.25 * p.dt * c->ph.qm;
+  P.magnetic = (c->ph.B[0] != 0 || c->ph.B[1] != 0 || c->ph.B[2] != 0);
+  double t2 = 0;
+  for (int d = 0; d < 3; ++d) {
+    P.t[d] = P.h * c->ph.B[d];
+    t2 += P.t[d] * P.t[d];
+  }
+  for (int d = 0; d < 3; ++d) P.s[d] = 2.0 * P.t[d] / (1.0 + t2);
+  P.has_ext = 0;
+  for (int i = 0; i < 9; ++i) {
+    P.A[i] = c->ph.A[i];
+    if (P.A[i] != 0) P.has_ext = 1;
+  }
+  for (int d = 0; d < 3; ++d) {
+    P.c[d] = c->ph.c[d];
+    if (P.c[d] != 0) P.has_ext = 1;
+  }
+  P.kicks = kicks;
+  P.drift = drift;
+  return P;
+}
+
+pif_status need_ready(pif_ctx c) {
+  if (!c) return fail(PIF_ERR_ARG, "null context");
+  if (!c->ws) return fail(PIF_ERR_STATE, "workspace not set (pif_set_workspace)");
+  if (!c->has_state) return fail(PIF_ERR_STATE, "state not set (pif_set_state)");
+  return PIF_OK;
+}
+
+// Phase events (only when profiling is on): a start/stop pair per phase call.
+pif_status ph_mark(pif_ctx c, int ph) {
+  if (!c->prof) return PIF_OK;
+  auto& v = c->ev[ph];
+  if (c->ev_used[ph] == v.size()) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    v.push_back(e);
+  }
+  CU(cudaEventRecord(v[c->ev_used[ph]++], c->st));
+  return PIF_OK;
+}
+#define PH(ph, body)            \
+  do {                          \
+    TRY(ph_mark(c, ph));        \
+    body;                       \
+    TRY(ph_mark(c, ph));        \
+  } while (0)
+
+// a0: counting sort of the working particles (xA, vA, idA) by brick of plan p.
+pif_status sort_particles(pif_ctx c, Plan& p) {
+  const int64_t n = c->nloc;
+  CU(cudaMemsetAsync(c->counts, 0, p.nbricks * sizeof(int), c->st));
+  CU(launch_bin_count(c->xA, n, n, p.g, c->key, c->rnk, c->counts, c->st));
+  CU(launch_scan(c->counts, c->offsets, p.nbricks, c->st));
+  CU(launch_scatter_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->xB,
+                           c->vB, c->idB, nullptr, c->st));
+  std::swap(c->xA, c->xB);
+  std::swap(c->vA, c->vB);
+  std::swap(c->idA, c->idB);
+  return PIF_OK;
+}
+
+// One field solve of plan `which` at the current positions followed by the
+// fused interpolation + push (kicks half kicks, optional drift).
+pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
+  Plan& p = c->plan[which];
+  const int64_t n = c->nloc;
+  PushArgs P = push_args(c, p, kicks, drift);
+  if (p.kind == PIF_PROP_PIF_NUFFT) {
+    PH(PH_SORT, TRY(sort_particles(c, p)));
+    PH(PH_SPREAD, {
+      CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
+      CU(launch_spread(c->xA, n, nullptr, 1.0, c->offsets, p.g, p.grid, c->st));
+    });
+    PH(PH_FFT_FWD, CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec)));
+    const double L = c->ph.L;
+    PH(PH_BOX, CU(launch_extract_box(p.spec, p.n, p.N, p.cor, c->q / (L * L * L), p.box, c->st)));
+    if (c->space_size > 1)
+      PH(PH_ALLREDUCE, NC(ncclAllReduce(p.box, p.box, 2 * p.box_elems(), ncclDouble, ncclSum,
+                                        c->comm_space, c->st)));
+    PH(PH_POISSON, CU(launch_poisson_pad(p.box, p.n, p.N, L, p.cor, p.S, p.G3, c->st)));
+    PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
+    PH(PH_INTERP_PUSH, CU(launch_interp_push(p.grid3, c->xA, c->vA, n, c->idA, nullptr,
+                                             c->offsets, p.g, P, c->st)));
+    c->launches += 7;  // bin, scan, scatter, spread, extract, poisson, interp_push
+    c->box_fresh = (which == 0) && !drift;
+  } else {
+    const int Ng = p.n;
+    const double h = c->ph.L / Ng;
+    PH(PH_PIC_DEPOSIT, {
+      CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
+      CU(launch_cic_deposit(c->xA, n, n, Ng, 1.0 / h, p.grid, c->st));
+    });
+    if (c->space_size > 1)
+      PH(PH_ALLREDUCE, NC(ncclAllReduce(p.grid, p.grid, p.grid_pts(), ncclDouble, ncclSum,
+                                        c->comm_space, c->st)));
+    PH(PH_FFT_FWD, CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec)));
+    double scale = c->q / (h * h * h) / (double)p.grid_pts();
+    PH(PH_POISSON, CU(launch_pic_poisson(p.spec, Ng, c->ph.L, scale, p.G3, c->st)));
+    PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
+    c->launches += 2;
+    if (kicks > 0 || drift) {
+      PH(PH_PIC_GATHER_PUSH, CU(launch_cic_gather_push(p.grid3, c->xA, c->vA, n, n, Ng, 1.0 / h,
+                                                       P, c->st)));
+      c->launches += 1;
+    }
+    c->box_fresh = (which == 0) && !drift;
+  }
+  return PIF_OK;
+}
+
+pif_status materialize(pif_ctx c) {
+  if (!c->pending) return PIF_OK;
+  TRY(solve_and_push(c, c->pending_plan, 1, 0));
+  c->pending = false;
+  return PIF_OK;
+}
+
+pif_status step_internal(pif_ctx c, int which, int64_t nsteps) {
+  if (nsteps <= 0) return PIF_OK;
+  if (c->pending && c->pending_plan != which) TRY(materialize(c));
+  for (int64_t s = 0; s < nsteps; ++s) {
+    TRY(solve_and_push(c, which, c->pending ? 2 : 1, 1));
+    c->pending = true;
+    c->pending_plan = which;
+  }
+  c->box_fresh = false;
+  return PIF_OK;
+}
+
+// Canonical-order state buffer: [x(3n) | v(3n) | flag(1)] doubles.
+struct State {
+  double* p = nullptr;
+};
+
+pif_status load_state(pif_ctx c, const double* s) {
+  const int64_t n = c->nloc;
+  CU(cudaMemcpyAsync(c->xA, s, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  CU(cudaMemcpyAsync(c->vA, s + 3 * n, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  CU(launch_iota(c->idA, n, c->st));
+  c->pending = false;
+  c->box_fresh = false;
+  c->has_state = true;
+  return PIF_OK;
+}
+
+pif_status store_state(pif_ctx c, double* s) {
+  TRY(materialize(c));
+  const int64_t n = c->nloc;
+  CU(launch_scatter_by_id(c->xA, c->vA, c->idA, n, n, s, s + 3 * n, c->st));
+  return PIF_OK;
+}
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* pif_last_error(void) { return g_err.c_str(); }
+
+pif_status pif_nccl_unique_id(void* out128) {
+  if (!out128) return fail(PIF_ERR_ARG, "null output");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+  return PIF_OK;
+}
+
+pif_status pif_init(const pif_physics* phys, const pif_propagator* fine,
+                    const pif_propagator* coarse, int64_t n_particles_global,
+                    const pif_dist* dist, pif_ctx* out) {
+  if (!phys || !fine || !dist || !out) return fail(PIF_ERR_ARG, "null argument");
+  if (!(phys->L > 0) || !std::isfinite(phys->L)) return fail(PIF_ERR_ARG, "L must be > 0");
+  if (phys->total_charge == 0 || !std::isfinite(phys->total_charge))
+    return fail(PIF_ERR_ARG, "total_charge must be nonzero");
+  if (n_particles_global < 1 || n_particles_global > (int64_t)1 << 31)
+    return fail(PIF_ERR_ARG, "n_particles_global must be in [1, 2^31]");
+  if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || dist->space_size < 1 ||
+      dist->world % dist->space_size)
+    return fail(PIF_ERR_CONFIG, "bad process layout (space_size must divide world)");
+  if (dist->world > 1 && !dist->nccl_id) return fail(PIF_ERR_ARG, "nccl_id required for world > 1");
+  TRY(validate_prop(fine));
+  if (coarse) TRY(validate_prop(coarse));
+  if (coarse && fine->kind == PIF_PROP_PIF_NUFFT && coarse->kind == PIF_PROP_PIF_NUFFT &&
+      coarse->tol < fine->tol)
+    return fail(PIF_ERR_CONFIG, "coarse tolerance must be >= fine tolerance");
+  pif_ctx c = new pif_ctx_s();
+  c->ph.L = phys->L;
+  c->ph.qm = phys->q_over_m;
+  c->ph.Q = phys->total_charge;
+  for (int d = 0; d < 3; ++d) {
+    c->ph.B[d] = phys->B_ext[d];
+    c->ph.c[d] = phys->E_ext_c[d];
+  }
+  for (int i = 0; i < 9; ++i) c->ph.A[i] = phys->E_ext_A[i];
+  c->Nglob = n_particles_global;
+  c->q = phys->total_charge / (double)n_particles_global;      // R6
+  c->m = std::fabs(phys->total_charge) / (double)n_particles_global;
+  c->device = dist->device;
+  c->rank = dist->rank;
+  c->world = dist->world;
+  c->space_size = dist->space_size;
+  c->time_size = dist->world / dist->space_size;
+  c->s_idx = dist->rank % dist->space_size;
+  c->t_idx = dist->rank / dist->space_size;
+  c->st = (cudaStream_t)dist->stream;
+  const int64_t base = n_particles_global / c->space_size, rem = n_particles_global % c->space_size;
+  c->nloc = base + (c->s_idx < rem ? 1 : 0);
+  c->first = c->s_idx * base + std::min<int64_t>(c->s_idx, rem);
+  auto bail = [&](pif_status s) {
+    std::string msg = g_err;
+    pif_finalize(c);
+    g_err = msg;
+    return s;
+  };
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(PIF_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  pif_status s = make_plan(c, 0, fine);
+  if (s != PIF_OK) return bail(s);
+  if (coarse) {
+    s = make_plan(c, 1, coarse);
+    if (s != PIF_OK) return bail(s);
+  }
+  e = cudaMallocHost(&c->host_red, 16 * sizeof(double));
+  if (e != cudaSuccess) {
+    fail(PIF_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+    return bail(PIF_ERR_CUDA);
+  }
+  if (c->world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, dist->nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm_world, c->world, id, c->rank);
+    if (r != ncclSuccess) {
+      fail(PIF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      return bail(PIF_ERR_NCCL);
+    }
+    // space group: same time index; time group: same space index.
+    r = ncclCommSplit(c->comm_world, c->t_idx, c->s_idx, &c->comm_space, nullptr);
+    if (r == ncclSuccess) r = ncclCommSplit(c->comm_world, c->s_idx, c->t_idx, &c->comm_time, nullptr);
+    if (r != ncclSuccess) {
+      fail(PIF_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+      return bail(PIF_ERR_NCCL);
+    }
+  }
+  *out = c;
+  return PIF_OK;
+}
+
+pif_status pif_local_count(pif_ctx c, int64_t* first, int64_t* count) {
+  if (!c || !first || !count) return fail(PIF_ERR_ARG, "null argument");
+  *first = c->first;
+  *count = c->nloc;
+  return PIF_OK;
+}
+
+pif_status pif_workspace_size(pif_ctx c, size_t* bytes) {
+  if (!c || !bytes) return fail(PIF_ERR_ARG, "null argument");
+  *bytes = layout(c, nullptr);
+  return PIF_OK;
+}
+
+pif_status pif_set_workspace(pif_ctx c, void* dptr, size_t bytes) {
+  if (!c || !dptr) return fail(PIF_ERR_ARG, "null argument");
+  if ((uintptr_t)dptr % 256) return fail(PIF_ERR_ARG, "workspace must be 256-byte aligned");
+  size_t need = layout(c, nullptr);
+  if (bytes < need) return fail(PIF_ERR_OOM, "workspace too small: need " + std::to_string(need));
+  layout(c, (char*)dptr);
+  c->ws = dptr;
+  c->ws_bytes = bytes;
+  for (int i = 0; i < 2; ++i) {
+    Plan& p = c->plan[i];
+    if (!p.valid) continue;
+    CUFFT(cufftSetWorkArea(p.fwd, c->fft_work));
+    CUFFT(cufftSetWorkArea(p.inv, c->fft_work));
+    if (p.kind == PIF_PROP_PIF_NUFFT) {
+      CU(cudaMemcpyAsync(p.cor, p.hcor.data(), (p.N + 1) * sizeof(double), cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(p.S, p.hS.data(), (p.N + 1) * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    }
+  }
+  CU(cudaStreamSynchronize(c->st));
+  c->has_state = false;
+  return PIF_OK;
+}
+
+pif_status pif_set_state(pif_ctx c, const double* x, const double* v, int64_t n_local,
+                         int on_device) {
+  if (!c || !x || !v) return fail(PIF_ERR_ARG, "null argument");
+  if (!c->ws) return fail(PIF_ERR_STATE, "workspace not set");
+  if (n_local != c->nloc) return fail(PIF_ERR_ARG, "n_local mismatch: expected " + std::to_string(c->nloc));
+  const size_t b = 3 * n_local * sizeof(double);
+  cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CU(cudaMemcpyAsync(c->xA, x, b, k, c->st));
+  CU(cudaMemcpyAsync(c->vA, v, b, k, c->st));
+  CU(launch_iota(c->idA, n_local, c->st));
+  if (!on_device) CU(cudaStreamSynchronize(c->st));
+  c->has_state = true;
+  c->pending = false;
+  c->box_fresh = false;
+  return PIF_OK;
+}
+
+pif_status pif_get_state(pif_ctx c, double* x, double* v, int64_t n_local, int on_device) {
+  TRY(need_ready(c));
+  if (!x || !v) return fail(PIF_ERR_ARG, "null argument");
+  if (n_local != c->nloc) return fail(PIF_ERR_ARG, "n_local mismatch");
+  TRY(materialize(c));
+  const int64_t n = c->nloc;
+  CU(launch_scatter_by_id(c->xA, c->vA, c->idA, n, n, c->xB, c->vB, c->st));
+  cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  CU(cudaMemcpyAsync(x, c->xB, 3 * n * sizeof(double), k, c->st));
+  CU(cudaMemcpyAsync(v, c->vB, 3 * n * sizeof(double), k, c->st));
+  if (!on_device) CU(cudaStreamSynchronize(c->st));
+  return PIF_OK;
+}
+
+pif_status pif_step(pif_ctx c, int which, int64_t n_steps) {
+  TRY(need_ready(c));
+  if (which < 0 || which > 1 || !c->plan[which].valid) return fail(PIF_ERR_ARG, "no such propagator");
+  if (n_steps < 0) return fail(PIF_ERR_ARG, "n_steps must be >= 0");
+  return step_internal(c, which, n_steps);
+}
+
+pif_status pif_field_energy(pif_ctx c, double W[3], double* kinetic, double momentum[3],
+                            double* charge_err) {
+  TRY(need_ready(c));
+  if (!W || !kinetic || !momentum || !charge_err) return fail(PIF_ERR_ARG, "null argument");
+  TRY(materialize(c));
+  Plan& p = c->plan[0];
+  if (!c->box_fresh) TRY(solve_and_push(c, 0, 0, 0));
+  const double L = c->ph.L;
+  if (p.kind == PIF_PROP_PIF_NUFFT) {
+    CU(launch_field_energy(p.box, p.N, L, p.S, c->red, c->st));
+  } else {
+    const double h = L / p.n;
+    CU(launch_grid_energy(p.grid3, p.grid_pts(), h * h * h, c->partials, c->red, c->st));
+  }
+  CU(launch_particle_moments(c->vA, c->nloc, c->nloc, c->partials, c->red + 4, c->st));
+  if (c->space_size > 1)
+    NC(ncclAllReduce(c->red + 4, c->red + 4, 4, ncclDouble, ncclSum, c->comm_space, c->st));
+  CU(cudaMemcpyAsync(c->host_red, c->red, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  const double* r = c->host_red;
+  if (p.kind == PIF_PROP_PIF_NUFFT) {
+    for (int d = 0; d < 3; ++d) W[d] = r[d];
+    *charge_err = std::fabs(L * L * L * r[3] - c->ph.Q) / std::fabs(c->ph.Q);
+  } else {
+    const double h = L / p.n;
+    for (int d = 0; d < 3; ++d) W[d] = 0.5 * h * h * h * r[d];
+    *charge_err = 0.0;
+  }
+  *kinetic = 0.5 * c->m * r[4];
+  for (int d = 0; d < 3; ++d) momentum[d] = c->m * r[5 + d];
+  return PIF_OK;
+}
+
+pif_status pif_plan_info(pif_ctx c, int which, int32_t* w, double* beta, int32_t* n_up) {
+  if (!c || which < 0 || which > 1 || !c->plan[which].valid) return fail(PIF_ERR_ARG, "bad plan");
+  const Plan& p = c->plan[which];
+  if (w) *w = p.kind == PIF_PROP_PIF_NUFFT ? p.g.w : 2;
+  if (beta) *beta = p.kind == PIF_PROP_PIF_NUFFT ? p.g.beta : 0.0;
+  if (n_up) *n_up = p.n;
+  return PIF_OK;
+}
+
+// ---------------------------------------------------------------- parareal --
+pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32_t max_iter,
+                        double stop_tol, int32_t n_blocks, pif_parareal_report* rep) {
+  TRY(need_ready(c));
+  if (!rep || !rep->retired_at || !rep->err_x || !rep->err_v) return fail(PIF_ERR_ARG, "null report");
+  if (!c->plan[1].valid) return fail(PIF_ERR_CONFIG, "parareal needs a coarse propagator");
+  if (n_slices < 1 || max_iter < 0 || !(t1 > t0)) return fail(PIF_ERR_ARG, "bad slices / iterations / interval");
+  if (n_blocks != 1) return fail(PIF_ERR_CONFIG, "n_blocks > 1 (windowed parareal) is not implemented");
+  if (c->time_size > 1 && n_slices != c->time_size)
+    return fail(PIF_ERR_CONFIG, "n_slices must equal the number of time ranks");
+  const double dT = (t1 - t0) / n_slices;
+  const int64_t nf = llround(dT / c->plan[0].dt), ng = llround(dT / c->plan[1].dt);
+  if (nf < 1 || ng < 1 || std::fabs(nf * c->plan[0].dt - dT) > 1e-9 * dT ||
+      std::fabs(ng * c->plan[1].dt - dT) > 1e-9 * dT)
+    return fail(PIF_ERR_CONFIG, "slice length must be an integer multiple of both dt");
+  const int64_t n = c->nloc, SZ = 6 * n + 1;
+  const double L = c->ph.L;
+  double tt0 = now();
+  double t_fine = 0, t_coarse = 0, t_comm = 0, t_coarse0 = 0;
+  for (int i = 0; i < max_iter * n_slices; ++i) rep->err_x[i] = rep->err_v[i] = NAN;
+  for (int i = 0; i < n_slices; ++i) rep->retired_at[i] = -1;
+
+  std::vector<double*> bufs;
+  auto alloc = [&](double** p) -> pif_status {
+    CU(cudaMallocAsync((void**)p, SZ * sizeof(double), c->st));
+    CU(cudaMemsetAsync(*p, 0, SZ * sizeof(double), c->st));
+    bufs.push_back(*p);
+    return PIF_OK;
+  };
+  auto free_all = [&]() {
+    for (double* b : bufs) cudaFreeAsync(b, c->st);
+    cudaStreamSynchronize(c->st);
+  };
+  auto timed = [&](double& acc, auto fn) -> pif_status {
+    CU(cudaStreamSynchronize(c->st));
+    double a = now();
+    pif_status s = fn();
+    if (s != PIF_OK) return s;
+    CU(cudaStreamSynchronize(c->st));
+    acc += now() - a;
+    return PIF_OK;
+  };
+  // propagate canonical state src -> canonical dst with plan `which`
+  auto propagate = [&](int which, const double* src, double* dst) -> pif_status {
+    TRY(load_state(c, src));
+    TRY(step_internal(c, which, which == 0 ? nf : ng));
+    TRY(store_state(c, dst));
+    return PIF_OK;
+  };
+  // correction + norms; errors (e_x, e_v) summed over the space group
+  auto correct = [&](const double* F, const double* Gn, const double* Go, double* U, double& ex,
+                     double& ev) -> pif_status {
+    CU(launch_correct_norms(F, Gn, Go, U, n, L, c->partials, c->red, c->st));
+    if (c->space_size > 1) NC(ncclAllReduce(c->red, c->red, 4, ncclDouble, ncclSum, c->comm_space, c->st));
+    CU(cudaMemcpyAsync(c->host_red, c->red, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    const double* r = c->host_red;
+    ex = r[1] > 0 ? std::sqrt(r[0] / r[1]) : std::sqrt(r[0]);
+    ev = r[3] > 0 ? std::sqrt(r[2] / r[3]) : std::sqrt(r[2]);
+    return PIF_OK;
+  };
+
+  pif_status st = PIF_OK;
+  int iterations = 0;
+  if (c->time_size == 1) {
+    // ---------------- reference schedule: all slices on this rank ----------
+    std::vector<double*> U(n_slices + 1), Gold(n_slices);
+    double *Fcur, *Fnext, *Gnew;
+    for (auto& p : U) if ((st = alloc(&p)) != PIF_OK) { free_all(); return st; }
+    for (auto& p : Gold) if ((st = alloc(&p)) != PIF_OK) { free_all(); return st; }
+    if ((st = alloc(&Fcur)) || (st = alloc(&Fnext)) || (st = alloc(&Gnew))) { free_all(); return st; }
+    std::vector<char> changed(n_slices, 1), retired(n_slices, 0);
+    st = store_state(c, U[0]);
+    // iteration 0: serial coarse sweep
+    for (int s = 0; s < n_slices && st == PIF_OK; ++s) {
+      st = timed(t_coarse0, [&] { return propagate(1, U[s], Gold[s]); });
+      changed[s] = 0;
+      if (st == PIF_OK) {
+        cudaError_t e = cudaMemcpyAsync(U[s + 1], Gold[s], SZ * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+        if (e != cudaSuccess) st = fail(PIF_ERR_CUDA, cudaGetErrorString(e));
+        if (s + 1 < n_slices) changed[s + 1] = 1;
+      }
+    }
+    for (int k = 0; k < max_iter && st == PIF_OK; ++k) {
+      int r0 = 0;
+      while (r0 < n_slices && retired[r0]) ++r0;
+      if (r0 == n_slices) break;
+      iterations = k + 1;
+      st = timed(t_fine, [&] { return propagate(0, U[r0], Fcur); });
+      for (int s = r0; s < n_slices && st == PIF_OK; ++s) {
+        if (s + 1 < n_slices) st = timed(t_fine, [&] { return propagate(0, U[s + 1], Fnext); });
+        if (st != PIF_OK) break;
+        double* Gn = Gold[s];
+        if (changed[s]) {
+          st = timed(t_coarse, [&] { return propagate(1, U[s], Gnew); });
+          if (st != PIF_OK) break;
+          Gn = Gnew;
+        }
+        double ex = 0, ev = 0;
+        st = correct(Fcur, Gn, Gold[s], U[s + 1], ex, ev);
+        if (st != PIF_OK) break;
+        if (s + 1 < n_slices) changed[s + 1] = 1;
+        changed[s] = 0;
+        if (Gn == Gnew) std::swap(Gold[s], Gnew);
+        rep->err_x[k * n_slices + s] = ex;
+        rep->err_v[k * n_slices + s] = ev;
+        if (ex <= stop_tol && ev <= stop_tol && (s == 0 || retired[s - 1])) {
+          retired[s] = 1;
+          rep->retired_at[s] = k + 1;
+        }
+        std::swap(Fcur, Fnext);
+      }
+    }
+    if (st == PIF_OK) st = load_state(c, U[n_slices]);
+    int conv = 1;
+    for (int s = 0; s < n_slices; ++s) conv &= retired[s];
+    rep->converged = conv;
+  } else {
+    // ---------------- pipelined: slice t_idx on this time rank -------------
+    const int t = c->t_idx, T = c->time_size;
+    double *U, *Fk, *Gold, *Gnew, *Unext;
+    if ((st = alloc(&U)) || (st = alloc(&Fk)) || (st = alloc(&Gold)) || (st = alloc(&Gnew)) ||
+        (st = alloc(&Unext))) {
+      free_all();
+      return st;
+    }
+    auto nsend = [&](const double* buf) -> pif_status {
+      NC(ncclSend(buf, SZ, ncclDouble, t + 1, c->comm_time, c->st));
+      return PIF_OK;
+    };
+    auto nrecv = [&](double* buf) -> pif_status {
+      NC(ncclRecv(buf, SZ, ncclDouble, t - 1, c->comm_time, c->st));
+      return PIF_OK;
+    };
+    bool pred_retired = (t == 0), retired = false, changed = true;
+    std::vector<double> myx(max_iter, NAN), myv(max_iter, NAN);
+    int my_ret = -1;
+    // iteration 0
+    if (t == 0) st = store_state(c, U);
+    else st = timed(t_comm, [&] { return nrecv(U); });
+    if (st == PIF_OK) st = timed(t_coarse0, [&] { return propagate(1, U, Gold); });
+    changed = false;
+    if (st == PIF_OK && t + 1 < T) st = timed(t_comm, [&] { return nsend(Gold); });
+    for (int k = 0; k < max_iter && st == PIF_OK && !retired; ++k) {
+      iterations = k + 1;
+      st = timed(t_fine, [&] { return propagate(0, U, Fk); });
+      if (st != PIF_OK) break;
+      if (!pred_retired) {
+        st = timed(t_comm, [&] { return nrecv(U); });
+        if (st != PIF_OK) break;
+        double flag = 0;
+        CU(cudaMemcpyAsync(&c->host_red[8], U + 6 * n, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        flag = c->host_red[8];
+        if (flag != 0.0) pred_retired = true;
+        changed = true;
+      }
+      double* Gn = Gold;
+      if (changed) {
+        st = timed(t_coarse, [&] { return propagate(1, U, Gnew); });
+        if (st != PIF_OK) break;
+        Gn = Gnew;
+      }
+      double ex = 0, ev = 0;
+      st = correct(Fk, Gn, Gold, Unext, ex, ev);
+      if (st != PIF_OK) break;
+      changed = false;
+      if (Gn == Gnew) std::swap(Gold, Gnew);
+      myx[k] = ex;
+      myv[k] = ev;
+      if (ex <= stop_tol && ev <= stop_tol && pred_retired) {
+        retired = true;
+        my_ret = k + 1;
+      }
+      double fl = retired ? 1.0 : 0.0;
+      CU(cudaMemcpyAsync(Unext + 6 * n, &fl, sizeof(double), cudaMemcpyHostToDevice, c->st));
+      if (t + 1 < T) st = timed(t_comm, [&] { return nsend(Unext); });
+    }
+    if (st == PIF_OK) st = load_state(c, Unext);
+    // gather the report over the time group (small)
+    if (st == PIF_OK && max_iter > 0) {
+      double* d = nullptr;
+      const int64_t rowsz = 2 * (int64_t)max_iter + 2;
+      CU(cudaMallocAsync((void**)&d, rowsz * (T + 1) * sizeof(double), c->st));
+      std::vector<double> row(rowsz);
+      for (int k = 0; k < max_iter; ++k) {
+        row[k] = myx[k];
+        row[max_iter + k] = myv[k];
+      }
+      row[2 * max_iter] = my_ret;
+      row[2 * max_iter + 1] = iterations;
+      CU(cudaMemcpyAsync(d, row.data(), rowsz * sizeof(double), cudaMemcpyHostToDevice, c->st));
+      NC(ncclAllGather(d, d + rowsz, rowsz, ncclDouble, c->comm_time, c->st));
+      std::vector<double> all(rowsz * T);
+      CU(cudaMemcpyAsync(all.data(), d + rowsz, rowsz * T * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CU(cudaStreamSynchronize(c->st));
+      cudaFreeAsync(d, c->st);
+      int conv = 1;
+      iterations = 0;
+      for (int s = 0; s < T; ++s) {
+        const double* r = &all[s * rowsz];
+        for (int k = 0; k < max_iter; ++k) {
+          rep->err_x[k * n_slices + s] = r[k];
+          rep->err_v[k * n_slices + s] = r[max_iter + k];
+        }
+        rep->retired_at[s] = (int)r[2 * max_iter];
+        conv &= rep->retired_at[s] > 0;
+        iterations = std::max(iterations, (int)r[2 * max_iter + 1]);
+      }
+      rep->converged = conv;
+    }
+  }
+  free_all();
+  if (st != PIF_OK) return st;
+  rep->iterations = iterations;
+  rep->t_coarse0 = t_coarse0;
+  rep->t_fine = t_fine;
+  rep->t_coarse = t_coarse;
+  rep->t_comm = t_comm;
+  rep->t_total = now() - tt0;
+  return PIF_OK;
+}
+
+pif_status pif_profile(pif_ctx c, int enable) {
+  if (!c) return fail(PIF_ERR_ARG, "null context");
+  c->prof = enable != 0;
+  return PIF_OK;
+}
+
+pif_status pif_profile_read(pif_ctx c, double* phase_ms, int32_t n_phases, int64_t* launches,
+                            int reset) {
+  if (!c || !phase_ms || !launches || n_phases < PIF_NPHASES)
+    return fail(PIF_ERR_ARG, "need phase_ms[PIF_NPHASES] and launches");
+  CU(cudaStreamSynchronize(c->st));
+  for (int ph = 0; ph < PIF_NPHASES; ++ph) {
+    double acc = 0;
+    for (size_t i = 0; i + 1 < c->ev_used[ph]; i += 2) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, c->ev[ph][i], c->ev[ph][i + 1]));
+      acc += ms;
+    }
+    phase_ms[ph] = acc;
+    if (reset) c->ev_used[ph] = 0;
+  }
+  for (int ph = PIF_NPHASES; ph < n_phases; ++ph) phase_ms[ph] = 0;
+  *launches = c->launches;
+  if (reset) c->launches = 0;
+  return PIF_OK;
+}
+
+pif_status pif_finalize(pif_ctx c) {
+  if (!c) return PIF_OK;
+  for (int ph = 0; ph < PIF_NPHASES; ++ph)
+    for (cudaEvent_t e : c->ev[ph]) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (c->plan[i].fwd) cufftDestroy(c->plan[i].fwd);
+    if (c->plan[i].inv) cufftDestroy(c->plan[i].inv);
+  }
+  if (c->comm_space) ncclCommDestroy(c->comm_space);
+  if (c->comm_time) ncclCommDestroy(c->comm_time);
+  if (c->comm_world) ncclCommDestroy(c->comm_world);
+  if (c->host_red) cudaFreeHost(c->host_red);
+  delete c;
+  return PIF_OK;
+}
+
+// ------------------------------------------------------------- debug/tests --
+pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, const double* s,
+                           double* out) {
+  if (!c || !x || !s || !out || n < 1) return fail(PIF_ERR_ARG, "null argument / empty input");
+  if (!c->ws) return fail(PIF_ERR_STATE, "workspace not set");
+  if (which < 0 || which > 1 || !c->plan[which].valid || c->plan[which].kind != PIF_PROP_PIF_NUFFT)
+    return fail(PIF_ERR_ARG, "not a PIF propagator");
+  Plan& p = c->plan[which];
+  double *dx, *dx2, *ds, *ds2;
+  int *id, *id2, *key, *rk, *counts, *offs;
+  double2* dout;
+  const int64_t N3 = (int64_t)p.N * p.N * p.N;
+  CU(cudaMalloc(&dx, 3 * n * sizeof(double)));
+  CU(cudaMalloc(&dx2, 3 * n * sizeof(double)));
+  CU(cudaMalloc(&ds, n * sizeof(double)));
+  CU(cudaMalloc(&ds2, n * sizeof(double)));
+  CU(cudaMalloc(&id, 4 * n * sizeof(int)));
+  id2 = id + n;
+  key = id + 2 * n;
+  rk = id + 3 * n;
+  CU(cudaMalloc(&counts, (2 * p.nbricks + 1) * sizeof(int)));
+  offs = counts + p.nbricks;
+  CU(cudaMalloc(&dout, N3 * sizeof(double2)));
+  CU(cudaMemcpyAsync(dx, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(ds, s, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CU(launch_iota(id, n, c->st));
+  CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
+  CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
+  CU(launch_scan(counts, offs, p.nbricks, c->st));
+  CU(launch_scatter_sorted(dx, nullptr, id, ds, n, n, key, rk, offs, dx2, nullptr, id2, ds2, c->st));
+  CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
+  CU(launch_spread(dx2, n, ds2, 1.0, offs, p.g, p.grid, c->st));
+  CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec));
+  CU(launch_debug_extract_KN(p.spec, p.n, p.N, p.cor, dout, c->st));
+  CU(cudaMemcpyAsync(out, dout, N3 * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  cudaFree(dx); cudaFree(dx2); cudaFree(ds); cudaFree(ds2); cudaFree(id); cudaFree(counts); cudaFree(dout);
+  return PIF_OK;
+}
+
+pif_status pif_debug_type2(pif_ctx c, int which, const double* cin, const double* x, int64_t n,
+                           double* out) {
+  if (!c || !x || !cin || !out || n < 1) return fail(PIF_ERR_ARG, "null argument / empty input");
+  if (!c->ws) return fail(PIF_ERR_STATE, "workspace not set");
+  if (which < 0 || which > 1 || !c->plan[which].valid || c->plan[which].kind != PIF_PROP_PIF_NUFFT)
+    return fail(PIF_ERR_ARG, "not a PIF propagator");
+  Plan& p = c->plan[which];
+  const int64_t N3 = (int64_t)p.N * p.N * p.N;
+  double *dx, *dx2, *E;
+  int *id, *id2, *key, *rk, *counts, *offs;
+  double2* dc;
+  CU(cudaMalloc(&dx, 3 * n * sizeof(double)));
+  CU(cudaMalloc(&dx2, 3 * n * sizeof(double)));
+  CU(cudaMalloc(&E, 3 * n * sizeof(double)));
+  CU(cudaMalloc(&id, 4 * n * sizeof(int)));
+  id2 = id + n;
+  key = id + 2 * n;
+  rk = id + 3 * n;
+  CU(cudaMalloc(&counts, (2 * p.nbricks + 1) * sizeof(int)));
+  offs = counts + p.nbricks;
+  CU(cudaMalloc(&dc, N3 * sizeof(double2)));
+  CU(cudaMemcpyAsync(dx, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(dc, cin, N3 * sizeof(double2), cudaMemcpyHostToDevice, c->st));
+  CU(launch_iota(id, n, c->st));
+  CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
+  CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
+  CU(launch_scan(counts, offs, p.nbricks, c->st));
+  CU(launch_scatter_sorted(dx, nullptr, id, nullptr, n, n, key, rk, offs, dx2, nullptr, id2, nullptr, c->st));
+  CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, c->st));
+  CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3));
+  PushArgs P = push_args(c, p, 0, 0);
+  CU(launch_interp_push(p.grid3, dx2, nullptr, n, id2, E, offs, p.g, P, c->st));
+  CU(cudaMemcpyAsync(out, E, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  cudaFree(dx); cudaFree(dx2); cudaFree(E); cudaFree(id); cudaFree(counts); cudaFree(dc);
+  return PIF_OK;
+}
+
+pif_status pif_debug_push(pif_ctx c, int which, double* x, double* v, const double* E, int64_t n,
+                          int kicks, int drift) {
+  if (!c || !x || !v || !E || n < 1) return fail(PIF_ERR_ARG, "null argument");
+  if (which < 0 || which > 1 || !c->plan[which].valid) return fail(PIF_ERR_ARG, "no such propagator");
+  if (kicks < 0 || kicks > 2) return fail(PIF_ERR_ARG, "kicks must be 0, 1 or 2");
+  double* d;
+  CU(cudaMalloc(&d, 9 * n * sizeof(double)));
+  CU(cudaMemcpyAsync(d, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(d + 3 * n, v, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(d + 6 * n, E, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  PushArgs P = push_args(c, c->plan[which], kicks, drift);
+  CU(launch_push_only(d, d + 3 * n, d + 6 * n, n, n, P, c->st));
+  CU(cudaMemcpyAsync(x, d, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaMemcpyAsync(v, d + 3 * n, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  cudaFree(d);
+  return PIF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// Internal declarations of the PIF library (not part of the ABI).
+// Citations: P:n = PAPER.md line n; Rn = reading n of DESIGN.md.
+#pragma once
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pif.h"
+
+namespace pif {
+
+// ---------------------------------------------------------------- physics --
+struct Phys {
+  double L, qm, Q;
+  double B[3];
+  double A[9];
+  double c[3];
+};
+
+// Geometry of the tile-owned ("brick") spreading / interpolation kernels.
+// The upsampled periodic grid n^3 is cut into bricks of b^3 cells; each CTA owns
+// one brick and an R^3 tile (R = b + w - 1) covering every window of the
+// brick's particles.  A particle's window is the w grid points
+// [a - hw, a - hw + w) around its anchor a (round(x~) for odd w, floor(x~) for
+// even w), hw = (w - 1) / 2, so |g - x~| <= w / 2 on the whole window.
+struct Brick {
+  int n;         // upsampled grid points per dimension
+  int w;         // kernel width (grid points)
+  int hw;        // (w - 1) / 2
+  int odd;       // w odd
+  int b;         // cells per brick per dimension
+  int nb;        // bricks per dimension = ceil(n / b)
+  int R;         // tile points per dimension
+  double scale;  // n / L (grid units per length)
+  double beta;   // ES shape parameter
+};
+
+// Anchor cell of coordinate xs (grid units) with the window rule above; xs is
+// shifted by -n / +n when the anchor wraps so that g - xs stays the true offset.
+__device__ __forceinline__ int anchor_of(double& xs, const Brick& g) {
+  int a = g.odd ? (int)floor(xs + 0.5) : (int)floor(xs);
+  if (a >= g.n) {
+    a -= g.n;
+    xs -= g.n;
+  } else if (a < 0) {
+    a += g.n;
+    xs += g.n;
+  }
+  return a;
+}
+
+// Exponential-of-semicircle kernel psi(t) = exp(beta (sqrt(1 - (2t/w)^2) - 1)),
+// |t| <= w/2 (reading R12; FINUFFT's kernel, P:135 via refs).
+__device__ __forceinline__ double es_kernel(double t, double two_over_w, double beta) {
+  double z = t * two_over_w;
+  double r = 1.0 - z * z;
+  return r > 0.0 ? exp(beta * (sqrt(r) - 1.0)) : (r == 0.0 ? exp(-beta) : 0.0);
+}
+
+__device__ __forceinline__ double wrapL(double x, double L) {
+  double y = x - L * floor(x / L);
+  return y >= L ? 0.0 : y;
+}
+
+// Boris half kick of size dt/2 (reading R7): h = dt/4 * q/m.
+__device__ __forceinline__ void kick_half(double& vx, double& vy, double& vz, double Ex, double Ey,
+                                          double Ez, double h, double tx, double ty, double tz,
+                                          double sx, double sy, double sz, bool magnetic) {
+  double mx = vx + h * Ex, my = vy + h * Ey, mz = vz + h * Ez;
+  if (magnetic) {
+    double px = mx + (my * tz - mz * ty);
+    double py = my + (mz * tx - mx * tz);
+    double pz = mz + (mx * ty - my * tx);
+    mx = mx + (py * sz - pz * sy);
+    my = my + (pz * sx - px * sz);
+    mz = mz + (px * sy - py * sx);
+  }
+  vx = mx + h * Ex;
+  vy = my + h * Ey;
+  vz = mz + h * Ez;
+}
+
+// Push parameters shared by all push kernels.
+struct PushArgs {
+  double L, dt, h;          // h = dt/4 * q/m
+  double t[3], s[3];        // Boris vectors
+  double A[9], c[3];        // E_ext = A x + c
+  int magnetic, has_ext;
+  int kicks;                // 0, 1 or 2 half kicks
+  int drift;                // 1: x <- wrap(x + dt v)
+};
+
+__device__ __forceinline__ void push_particle(double& x0, double& x1, double& x2, double& v0,
+                                              double& v1, double& v2, double E0, double E1,
+                                              double E2, const PushArgs& P) {
+  if (P.has_ext) {
+    E0 += P.A[0] * x0 + P.A[1] * x1 + P.A[2] * x2 + P.c[0];
+    E1 += P.A[3] * x0 + P.A[4] * x1 + P.A[5] * x2 + P.c[1];
+    E2 += P.A[6] * x0 + P.A[7] * x1 + P.A[8] * x2 + P.c[2];
+  }
+  bool mag = P.magnetic != 0;
+  for (int k = 0; k < P.kicks; ++k)
+    kick_half(v0, v1, v2, E0, E1, E2, P.h, P.t[0], P.t[1], P.t[2], P.s[0], P.s[1], P.s[2], mag);
+  if (P.drift) {
+    x0 = wrapL(x0 + P.dt * v0, P.L);
+    x1 = wrapL(x1 + P.dt * v1, P.L);
+    x2 = wrapL(x2 + P.dt * v2, P.L);
+  }
+}
+
+// -------------------------------------------------------------- launchers --
+// All launchers enqueue on `st` and return cudaGetLastError().
+cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const Brick& g, int* key,
+                             int* rank, int* counts, cudaStream_t st);
+cudaError_t launch_scan(const int* counts, int* offsets, int64_t nbins, cudaStream_t st);
+cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,
+                                  int64_t stride, int64_t n, const int* key, const int* rank,
+                                  const int* offsets, double* x2, double* v2, int* id2, double* s2,
+                                  cudaStream_t st);
+cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
+                          const int* offsets, const Brick& g, double* grid, cudaStream_t st);
+cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
+                               const int* id, double* Eout, const int* offsets, const Brick& g,
+                               const PushArgs& P, cudaStream_t st);
+cudaError_t launch_extract_box(const double2* spec, int n, int N, const double* cor, double scale,
+                               double2* box, cudaStream_t st);
+cudaError_t launch_poisson_pad(const double2* box, int n, int N, double L, const double* cor,
+                               const double* S, double2* G3, cudaStream_t st);
+cudaError_t launch_debug_extract_KN(const double2* spec, int n, int N, const double* cor,
+                                    double2* out, cudaStream_t st);
+cudaError_t launch_debug_pad_KN(const double2* c, int n, int N, const double* cor, double2* G3,
+                                cudaStream_t st);
+cudaError_t launch_field_energy(const double2* box, int N, double L, const double* S,
+                                double* out4, cudaStream_t st);
+cudaError_t launch_particle_moments(const double* v, int64_t stride, int64_t n, double* partials,
+                                    double* out4, cudaStream_t st);
+cudaError_t launch_cic_deposit(const double* x, int64_t stride, int64_t n, int Ng, double inv_h,
+                               double* grid, cudaStream_t st);
+cudaError_t launch_pic_poisson(const double2* spec, int Ng, double L, double scale, double2* G3,
+                               cudaStream_t st);
+cudaError_t launch_cic_gather_push(const double* grid3, double* x, double* v, int64_t stride,
+                                   int64_t n, int Ng, double inv_h, const PushArgs& P,
+                                   cudaStream_t st);
+cudaError_t launch_grid_energy(const double* grid3, int64_t npts, double h3, double* partials,
+                               double* out4, cudaStream_t st);
+cudaError_t launch_push_only(double* x, double* v, const double* E, int64_t stride, int64_t n,
+                             const PushArgs& P, cudaStream_t st);
+cudaError_t launch_scatter_by_id(const double* x, const double* v, const int* id, int64_t stride,
+                                 int64_t n, double* xo, double* vo, cudaStream_t st);
+cudaError_t launch_iota(int* id, int64_t n, cudaStream_t st);
+cudaError_t launch_correct_norms(const double* F, const double* Gn, const double* Go, double* U,
+                                 int64_t n, double L, double* partials, double* out4,
+                                 cudaStream_t st);
+cudaError_t launch_check_finite(const double* a, int64_t count, int* flag, cudaStream_t st);
+
+constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
+}  // namespace pif

@@ -1,0 +1,130 @@
+// a0: bin particles by brick and counting-sort them physically (SoA x, v, id).
+// Not a method step (cuFINUFFT bins internally); it gives the brick
+// kernels contiguous, coalesced particle ranges per CTA.
+#include "pif_internal.cuh"
+
+namespace pif {
+
+__global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_t n, Brick g,
+                            int* __restrict__ key, int* __restrict__ rank,
+                            int* __restrict__ counts) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int B[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double xs = x[d * stride + j] * g.scale;
+    int a = anchor_of(xs, g);
+    B[d] = a / g.b;
+  }
+  int k = (B[0] * g.nb + B[1]) * g.nb + B[2];
+  key[j] = k;
+  rank[j] = atomicAdd(&counts[k], 1);
+}
+
+// Exclusive scan of counts[0..nbins) into offsets[0..nbins] with one CTA of
+// 1024 threads (nbins <= 2^20): per-thread serial chunk + block scan of sums.
+__global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ counts,
+                                               int* __restrict__ offsets, int64_t nbins) {
+  __shared__ int warp_sums[32];
+  const int T = blockDim.x, t = threadIdx.x;
+  const int64_t per = (nbins + T - 1) / T;
+  const int64_t lo = t * per, hi = min(nbins, lo + per);
+  int local = 0;
+  for (int64_t i = lo; i < hi; ++i) local += counts[i];
+  // inclusive scan of `local` across the block
+  int lane = t & 31, wid = t >> 5;
+  int v = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) warp_sums[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int w = (lane < (T >> 5)) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    warp_sums[lane] = w;
+  }
+  __syncthreads();
+  int excl = v - local + (wid > 0 ? warp_sums[wid - 1] : 0);
+  for (int64_t i = lo; i < hi; ++i) {
+    offsets[i] = excl;
+    excl += counts[i];
+  }
+  if (t == T - 1) offsets[nbins] = excl;
+}
+
+__global__ void k_scatter_sorted(const double* __restrict__ x, const double* __restrict__ v,
+                                 const int* __restrict__ id, const double* __restrict__ s,
+                                 int64_t stride, int64_t n, const int* __restrict__ key,
+                                 const int* __restrict__ rank, const int* __restrict__ offsets,
+                                 double* __restrict__ x2, double* __restrict__ v2,
+                                 int* __restrict__ id2, double* __restrict__ s2) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t dst = offsets[key[j]] + rank[j];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    x2[d * stride + dst] = x[d * stride + j];
+    if (v) v2[d * stride + dst] = v[d * stride + j];
+  }
+  id2[dst] = id[j];
+  if (s) s2[dst] = s[j];
+}
+
+__global__ void k_iota(int* id, int64_t n) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) id[j] = (int)j;
+}
+
+// dst (canonical order) <- src (sorted order) by particle id.
+__global__ void k_scatter_by_id(const double* __restrict__ x, const double* __restrict__ v,
+                                const int* __restrict__ id, int64_t stride, int64_t n,
+                                double* __restrict__ xo, double* __restrict__ vo) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t k = id[j];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    xo[d * stride + k] = x[d * stride + j];
+    vo[d * stride + k] = v[d * stride + j];
+  }
+}
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const Brick& g, int* key,
+                             int* rank, int* counts, cudaStream_t st) {
+  if (n > 0) k_bin_count<<<nblk(n, 256), 256, 0, st>>>(x, stride, n, g, key, rank, counts);
+  return cudaGetLastError();
+}
+cudaError_t launch_scan(const int* counts, int* offsets, int64_t nbins, cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(counts, offsets, nbins);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,
+                                  int64_t stride, int64_t n, const int* key, const int* rank,
+                                  const int* offsets, double* x2, double* v2, int* id2, double* s2,
+                                  cudaStream_t st) {
+  if (n > 0)
+    k_scatter_sorted<<<nblk(n, 256), 256, 0, st>>>(x, v, id, s, stride, n, key, rank, offsets, x2,
+                                                   v2, id2, s2);
+  return cudaGetLastError();
+}
+cudaError_t launch_iota(int* id, int64_t n, cudaStream_t st) {
+  if (n > 0) k_iota<<<nblk(n, 256), 256, 0, st>>>(id, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter_by_id(const double* x, const double* v, const int* id, int64_t stride,
+                                 int64_t n, double* xo, double* vo, cudaStream_t st) {
+  if (n > 0) k_scatter_by_id<<<nblk(n, 256), 256, 0, st>>>(x, v, id, stride, n, xo, vo);
+  return cudaGetLastError();
+}
+
+}  // namespace pif

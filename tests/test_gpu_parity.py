@@ -1,0 +1,251 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star):
+* NUFFT type-1 / type-2 relative L2 error vs the direct NUDFT <= 10 eps;
+* positions, velocities, field energy <= 1e-10 relative after 20 fine steps;
+* CIC-PIC (an exact algorithm on both sides) <= 1e-12 after 20 steps;
+* momentum drift <= 1e-13 sum m|v|.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from pif_inputs import landau_physics, landau_state, penning_physics, penning_state, tsi_physics, tsi_state
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2407_00485_b200 as P  # noqa: E402
+
+
+def sim_for(phys, fine, coarse=None, n=1):
+    return P.Simulation(P.physics(phys.L, phys.q_over_m, phys.total_charge, phys.B, phys.A, phys.c),
+                        fine, coarse, n_particles=n)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+# ------------------------------------------------------------ transforms ---
+@pytest.mark.parametrize("tol", [1e-12, 1e-7, 1e-4])
+@pytest.mark.parametrize("signed", [False, True])
+def test_type1_vs_nudft_C1(tol, signed):
+    """C1 inputs (Landau, 8^3 modes, 16384 particles)."""
+    phys = landau_physics()
+    x, _ = landau_state(16384, 0)
+    s = np.random.default_rng(1).standard_normal(16384) if signed else np.ones(16384)
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=tol), n=16384)
+    got = P.pif_debug_type1(sim.ctx, 0, x, s, 8)
+    ref = O.nudft_type1(x, s, 8, phys.L)
+    assert rel_l2(got, ref) <= 10 * tol
+
+
+@pytest.mark.parametrize("tol", [1e-12, 1e-7, 1e-4])
+def test_type2_vs_nudft_C1(tol):
+    phys = landau_physics()
+    x, _ = landau_state(16384, 0)
+    rng = np.random.default_rng(2)
+    c = rng.standard_normal((8, 8, 8)) + 1j * rng.standard_normal((8, 8, 8))
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=tol), n=16384)
+    got = P.pif_debug_type2(sim.ctx, 0, c, x)
+    ref = O.nudft_type2(c, x, 8, phys.L)
+    assert rel_l2(got, ref) <= 10 * tol
+
+
+@pytest.mark.parametrize("N,npart", [(2, 1), (6, 37), (16, 5000), (32, 20000)])
+def test_type1_type2_ragged_and_edge_sizes(N, npart):
+    """Tiny / ragged particle counts, N = 2 (only Nyquist and k=0), larger N."""
+    phys = penning_physics()
+    rng = np.random.default_rng(N)
+    x = rng.random((3, npart)) * phys.L
+    x[:, 0] = [0.0, phys.L * (1 - 1e-16), phys.L / 2]  # edge positions
+    s = rng.standard_normal(npart)
+    c = rng.standard_normal((N, N, N)) + 1j * rng.standard_normal((N, N, N))
+    sim = sim_for(phys, P.propagator("pif", N, 0.01, tol=1e-12), n=npart)
+    assert rel_l2(P.pif_debug_type1(sim.ctx, 0, x, s, N), O.nudft_type1(x, s, N, phys.L)) <= 1e-11
+    assert rel_l2(P.pif_debug_type2(sim.ctx, 0, c, x), O.nudft_type2(c, x, N, phys.L)) <= 1e-11
+
+
+def test_type1_type2_adjoint_pair():
+    """The GPU type-1/type-2 pair is adjoint to rounding (same kernel, w, n, psi^):
+    the basis of momentum conservation at any eps."""
+    phys = landau_physics()
+    rng = np.random.default_rng(3)
+    x = rng.random((3, 3000)) * phys.L
+    s = rng.standard_normal(3000)
+    c = rng.standard_normal((8, 8, 8)) + 1j * rng.standard_normal((8, 8, 8))
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=1e-4), n=3000)
+    lhs = np.real(np.vdot(c, P.pif_debug_type1(sim.ctx, 0, x, s, 8)))
+    rhs = float(s @ P.pif_debug_type2(sim.ctx, 0, c, x))
+    assert abs(lhs - rhs) <= 1e-13 * np.abs(s).sum() * np.abs(c).sum()
+
+
+# ------------------------------------------------------------------- push --
+@pytest.mark.parametrize("case", ["landau", "penning"])
+@pytest.mark.parametrize("kicks,drift", [(1, 1), (2, 1), (1, 0)])
+def test_push_vs_oracle(case, kicks, drift):
+    phys = penning_physics() if case == "penning" else landau_physics()
+    x, v = (penning_state if case == "penning" else landau_state)(1000, 4)
+    E = np.random.default_rng(5).standard_normal((3, 1000))
+    sim = sim_for(phys, P.propagator("pif", 8, 0.003125, tol=1e-7), n=1000)
+    xg, vg = x.copy(), v.copy()
+    P.pif_debug_push(sim.ctx, 0, xg, vg, E, kicks, drift)
+    ph = O.PhysicsParams.from_inputs(phys)
+    Et = E + O.external_field(x, ph.A, ph.c)
+    vr = v
+    for _ in range(kicks):
+        vr = O.kick_half(vr, Et, 0.003125, ph.q_over_m, ph.B)
+    xr = O.wrap(x + 0.003125 * vr, ph.L) if drift else x
+    assert np.abs(vg - vr).max() <= 1e-15 * np.abs(vr).max() * 4
+    assert np.abs(O.min_image(xg - xr, ph.L)).max() <= 1e-15 * ph.L * 4
+
+
+# ------------------------------------------------------------- full steps --
+def run_gpu(phys, fine, x0, v0, steps, coarse=None, which=0):
+    sim = sim_for(phys, fine, coarse, n=x0.shape[1])
+    sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
+    sim.step(steps, which)
+    x, v = sim.get_state()
+    W, ke, mom, ce = sim.field_energy()
+    return x.cpu().numpy(), v.cpu().numpy(), W, ke, mom, ce, sim
+
+
+@pytest.mark.parametrize("case,N,npart,dt", [
+    ("landau", 8, 16384, 0.05),    # C1
+    ("tsi", 8, 4096, 0.05),
+    ("penning", 8, 4096, 0.003125),
+])
+def test_fine_steps_vs_oracle(case, N, npart, dt):
+    """20 fine PIF steps (tol 1e-12) vs the exact NUDFT PIF: x, v, W <= 1e-10 rel."""
+    phys = {"landau": landau_physics, "tsi": tsi_physics, "penning": penning_physics}[case]()
+    x0, v0 = {"landau": landau_state, "tsi": tsi_state, "penning": penning_state}[case](npart, 0)
+    steps = 20
+    x, v, W, ke, mom, ce, _ = run_gpu(phys, P.propagator("pif", N, dt, tol=1e-12), x0, v0, steps)
+    ph = O.PhysicsParams.from_inputs(phys)
+    prop = O.Propagator("pif", N, dt)
+    xr, vr = O.run(x0, v0, steps, prop, ph)
+    assert np.abs(O.min_image(x - xr, phys.L)).max() <= 1e-10 * phys.L
+    assert np.abs(v - vr).max() <= 1e-10 * np.abs(vr).max()
+    Wr, ker, momr, cer = O.diagnostics(xr, vr, prop, ph)
+    assert np.all(np.abs(W - Wr) <= 1e-10 * Wr.sum())
+    assert abs(ke - ker) <= 1e-10 * ker
+    assert ce <= 1e-10
+
+
+def test_momentum_conservation_any_tolerance():
+    """Momentum drift <= 1e-13 sum m|v| for eps = 1e-4."""
+    phys = landau_physics()
+    x0, v0 = landau_state(20000, 6)
+    for tol in (1e-4, 1e-12):
+        x, v, W, ke, mom, ce, sim = run_gpu(phys, P.propagator("pif", 8, 0.05, tol=tol), x0, v0, 50)
+        m = abs(phys.total_charge) / 20000
+        mom0 = m * v0.sum(axis=1)
+        scale = m * np.abs(v0).sum()
+        assert np.abs(mom - mom0).max() <= 1e-13 * scale, (tol, mom - mom0)
+
+
+def test_pic_steps_vs_oracle():
+    """20 CIC-PIC steps (exact algorithm on both sides) <= 1e-12."""
+    phys = landau_physics()
+    x0, v0 = landau_state(8192, 7)
+    x, v, *_ = run_gpu(phys, P.propagator("pic", 16, 0.05), x0, v0, 20)
+    xr, vr = O.run(x0, v0, 20, O.Propagator("pic", 16, 0.05), O.PhysicsParams.from_inputs(phys))
+    assert np.abs(O.min_image(x - xr, phys.L)).max() <= 1e-12 * phys.L
+    assert np.abs(v - vr).max() <= 1e-12 * np.abs(vr).max()
+
+
+def test_fine_then_coarse_switch_and_lazy_kick():
+    """Mixed fine/coarse stepping and repeated get_state equal the oracle sequence."""
+    phys = landau_physics()
+    ph = O.PhysicsParams.from_inputs(phys)
+    x0, v0 = landau_state(4096, 8)
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=1e-12), P.propagator("pic", 16, 0.1), n=4096)
+    sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
+    sim.step(3, 0)
+    sim.get_state()
+    sim.step(2, 1)
+    sim.step(2, 0)
+    x, v = sim.get_state()
+    xr, vr = O.run(x0, v0, 3, O.Propagator("pif", 8, 0.05), ph)
+    xr, vr = O.run(xr, vr, 2, O.Propagator("pic", 16, 0.1), ph)
+    xr, vr = O.run(xr, vr, 2, O.Propagator("pif", 8, 0.05), ph)
+    assert np.abs(O.min_image(x.cpu().numpy() - xr, phys.L)).max() <= 1e-10 * phys.L
+    assert np.abs(v.cpu().numpy() - vr).max() <= 1e-10 * np.abs(vr).max()
+
+
+# --------------------------------------------------------------- parareal --
+def test_parareal_matches_oracle_trace_pic_coarse():
+    """Serial-schedule parareal on the GPU (F = PIF 1e-12, G = CIC-PIC) vs the
+    oracle's parareal: same retirement pattern and per-iteration errors."""
+    phys = landau_physics()
+    ph = O.PhysicsParams.from_inputs(phys)
+    x0, v0 = landau_state(2048, 9)
+    Ns, nf, ng = 4, 4, 2
+    fine = P.propagator("pif", 8, 0.05, tol=1e-12)
+    coarse = P.propagator("pic", 8, 0.1)
+    sim = sim_for(phys, fine, coarse, n=2048)
+    sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
+    rep = sim.parareal(0.0, Ns * nf * 0.05, Ns, Ns, 1e-6)
+    x, v = sim.get_state()
+    F = O.make_propagator_fn(O.Propagator("pif", 8, 0.05), ph, nf)
+    G = O.make_propagator_fn(O.Propagator("pic", 8, 0.1), ph, ng)
+    ref = O.parareal_serial((x0, v0), F, G, Ns, Ns, 1e-6, L=phys.L)
+    assert rep["retired_at"] == ref.retired_at
+    assert rep["iterations"] == ref.iterations
+    ex_ref = np.array(ref.err_x)
+    got = rep["err_x"][: ref.iterations]
+    fin = np.isfinite(ex_ref)
+    assert np.array_equal(fin, np.isfinite(got))
+    assert np.allclose(got[fin], ex_ref[fin], rtol=1e-6, atol=1e-12)
+    xs, vs = ref.U[Ns]
+    assert np.abs(O.min_image(x.cpu().numpy() - xs, phys.L)).max() <= 1e-9 * phys.L
+
+
+def test_parareal_tol0_equals_serial_fine():
+    """max_iter = N_s, tol = 0: U_Ns equals the GPU serial fine run (<= 1e-12)."""
+    phys = landau_physics()
+    x0, v0 = landau_state(4096, 10)
+    Ns, nf = 4, 3
+    fine = P.propagator("pif", 8, 0.05, tol=1e-12)
+    coarse = P.propagator("pif", 8, 0.15, tol=1e-4)
+    sim = sim_for(phys, fine, coarse, n=4096)
+    sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
+    rep = sim.parareal(0.0, Ns * nf * 0.05, Ns, Ns, 0.0)
+    x, v = sim.get_state()
+    assert rep["retired_at"] == [1, 2, 3, 4] and rep["converged"]
+    sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
+    sim.step(Ns * nf)
+    xs, vs = sim.get_state()
+    dx = O.min_image((x - xs).cpu().numpy(), phys.L)
+    assert np.abs(dx).max() <= 1e-12 * phys.L
+    assert (v - vs).abs().max().item() <= 1e-12 * vs.abs().max().item()
+
+
+# ------------------------------------------------------- full-size checks --
+def test_C2_full_size_sampled_modes_and_particles():
+    """BASELINE configs[1] size (Landau 32^3 modes, 2^21 particles, tol 1e-12) in
+    the bench's launch configuration: type-1 on 64 sampled modes against the
+    per-mode direct sum, type-2 on 512 sampled particles."""
+    phys = landau_physics()
+    n = 1 << 21
+    x, _ = landau_state(n, 1)
+    N = 32
+    sim = sim_for(phys, P.propagator("pif", N, 0.05, tol=1e-12), n=n)
+    s = np.random.default_rng(11).standard_normal(n)
+    got = P.pif_debug_type1(sim.ctx, 0, x, s, N)
+    rng = np.random.default_rng(12)
+    idx = rng.integers(0, N, size=(64, 3))
+    k = 2 * math.pi / phys.L * (idx - N // 2)
+    ref = np.array([np.sum(s * np.exp(-1j * (kk @ x))) for kk in k])
+    g = got[idx[:, 0], idx[:, 1], idx[:, 2]]
+    assert rel_l2(g, ref) <= 10 * 1e-12
+    c = rng.standard_normal((N, N, N)) + 1j * rng.standard_normal((N, N, N))
+    sel = rng.choice(n, 512, replace=False)
+    out = P.pif_debug_type2(sim.ctx, 0, c, x)
+    assert rel_l2(out[sel], O.nudft_type2(c, x[:, sel], N, phys.L)) <= 10 * 1e-12
