@@ -224,19 +224,32 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     int w = es_width(pr->tol);
     int n = 2;
     while (n < std::max(2 * pr->n, 2 * w)) n *= 2;
-    int R = (w + 3 <= 8) ? 8 : (w + 3 <= 12) ? 12 : 16;
+    // Tile shapes (DMMA needs RZ % 8 == 0 for spreading and
+    // (RX RY) % 32 == 0).  w = 13 (eps = 1e-12): interpolation tiles 16x14x16
+    // over 4x2x4-cell sub-bricks, spreading tiles 16^3 over 4^3-cell bricks.
+    int RI[3], m[3] = {1, 1, 1};
+    if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
+    else if (w <= 12 || w > 13) { RI[0] = RI[1] = RI[2] = 16; }
+    else { RI[0] = 16; RI[1] = 14; RI[2] = 16; m[1] = 2; }
     Brick& g = p.g;
     g.n = n;
     g.w = w;
     g.hw = (w - 1) / 2;
     g.odd = w & 1;
-    g.R = R;
-    g.b = R - w + 1;
-    g.nb = (n + g.b - 1) / g.b;
+    g.nkeys = 1;
+    for (int d = 0; d < 3; ++d) {
+      g.RI[d] = RI[d];
+      g.ib[d] = RI[d] - w + 1;
+      g.m[d] = m[d];
+      g.sb[d] = g.ib[d] * m[d];
+      g.RS[d] = g.sb[d] + w - 1;
+      g.NB[d] = (n + g.sb[d] - 1) / g.sb[d];
+      g.nkeys *= (int64_t)g.NB[d] * m[d];
+    }
     g.scale = n / L;
     g.beta = es_beta(w);
     p.n = n;
-    p.nbricks = (int64_t)g.nb * g.nb * g.nb;
+    p.nbricks = g.nkeys;
     c->max_bins = std::max(c->max_bins, p.nbricks);
     const int H = p.N / 2;
     p.hcor.resize(p.N + 1);

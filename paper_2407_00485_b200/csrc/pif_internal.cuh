@@ -20,20 +20,27 @@ struct Phys {
   double c[3];
 };
 
-// Geometry of the tile-owned ("brick") spreading / interpolation kernels.
-// The upsampled periodic grid n^3 is cut into bricks of b^3 cells; each CTA owns
-// one brick and an R^3 tile (R = b + w - 1) covering every window of the
-// brick's particles.  A particle's window is the w grid points
-// [a - hw, a - hw + w) around its anchor a (round(x~) for odd w, floor(x~) for
-// even w), hw = (w - 1) / 2, so |g - x~| <= w / 2 on the whole window.
+// Geometry of the tile-owned spreading / interpolation kernels.  The upsampled
+// periodic grid n^3 is cut into interpolation sub-bricks of ib[d] cells; m[d]
+// sub-bricks per dimension form a spreading brick of sb[d] = m[d] ib[d] cells.
+// A CTA owns the tile covering every window of its cells: RI = ib + w - 1
+// (interpolation) or RS = sb + w - 1 (spreading) points per dimension.  A
+// particle's window is the w grid points [a - hw, a - hw + w) around its anchor
+// a (round(x~) for odd w, floor(x~) for even w), hw = (w - 1) / 2, so that
+// |g - x~| <= w / 2 on the whole window.  Sort key (brick-major):
+// key = brick * (m0 m1 m2) + sub-brick-in-brick.
 struct Brick {
   int n;         // upsampled grid points per dimension
   int w;         // kernel width (grid points)
   int hw;        // (w - 1) / 2
   int odd;       // w odd
-  int b;         // cells per brick per dimension
-  int nb;        // bricks per dimension = ceil(n / b)
-  int R;         // tile points per dimension
+  int ib[3];     // cells per interpolation sub-brick
+  int m[3];      // sub-bricks per spreading brick
+  int sb[3];     // cells per spreading brick
+  int NB[3];     // spreading bricks per dimension = ceil(n / sb)
+  int RI[3];     // interpolation tile points
+  int RS[3];     // spreading tile points
+  int64_t nkeys; // number of sub-bricks = NB0 NB1 NB2 m0 m1 m2
   double scale;  // n / L (grid units per length)
   double beta;   // ES shape parameter
 };

@@ -10,14 +10,16 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
                             int* __restrict__ counts) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
-  int B[3];
+  int B[3], S[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     double xs = x[d * stride + j] * g.scale;
     int a = anchor_of(xs, g);
-    B[d] = a / g.b;
+    B[d] = a / g.sb[d];
+    S[d] = (a - B[d] * g.sb[d]) / g.ib[d];
   }
-  int k = (B[0] * g.nb + B[1]) * g.nb + B[2];
+  int k = ((B[0] * g.NB[1] + B[1]) * g.NB[2] + B[2]) * (g.m[0] * g.m[1] * g.m[2]) +
+          (S[0] * g.m[1] + S[1]) * g.m[2] + S[2];
   key[j] = k;
   rank[j] = atomicAdd(&counts[k], 1);
 }

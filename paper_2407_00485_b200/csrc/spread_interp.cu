@@ -1,183 +1,321 @@
-// a1 (type-1 spread) and a7+a8 (type-2 interpolation fused with the push).
+// a1 (type-1 spread) and a7+a8 (type-2 interpolation fused with the push) on
+// the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64; 37 TFLOP/s measured on
+// B200 -- tcgen05 has no f64 kind).
 //
-// Tile-owned design: one CTA per brick of b^3 cells;
-// thread (tx, ty) owns the z-column (T0x+tx, T0y+ty, T0z .. T0z+R-1) of the
-// brick's R^3 tile.  Spreading accumulates each column in R registers over all
-// particles of the brick (no shared-memory atomics -- fp64 smem atomicAdd is a
-// CAS loop on sm_100a) and flushes the tile once with native fp64 global
-// reductions (REDG.ADD.F64 resolved in L2).  Interpolation holds the three
-// field components of the column in registers and reduces the per-column
-// partial sums of each particle across the CTA.
+// Tile-owned design: the upsampled grid is cut into
+// sub-bricks of ib cells (interpolation CTAs) grouped m at a time into bricks
+// (spreading CTAs); particles are counting-sorted brick-major so a brick's
+// particles are the concatenation of its sub-bricks'.  A CTA owns the
+// RX x RY x RZ tile that covers every w-point window of its cells.  With
+// columns c = (cx, cy) (c = cy*RX + cx) and separable ES weights
+// psi_x[p][cx] psi_y[p][cy] psi_z[p][z] (reading R12; zero outside the
+// particle's window) both transforms are dense contractions over the tile:
 //
-// Separable ES weights (reading R12): psi_d[t] = psi(T0_d + t - x~_d) inside
-// the particle's w-point window, 0 outside, computed once per particle and
-// staged in shared memory.
+//   spread:  G[c][z]   += sum_p W[c][p] psi_z[p][z],  W[c][p] = psi_x[p][cx] psi_y[p][cy]
+//            (M = columns, N = z, K = particles; the tile lives in the MMA
+//            accumulators over all particles of the brick and is flushed once
+//            with native fp64 global reductions, REDG.ADD.F64, into the
+//            L2-resident grid -- no shared-memory atomics, which are CAS loops
+//            for fp64 on sm_100a);
+//   interp:  T_d[p][c]  = sum_z psi_z[p][z] g_d[z][c]     (M = particles, N = columns,
+//            K = z; the 3 field components of the tile stay in registers as B
+//            fragments for the whole sub-brick), then
+//            E_d[p] = sum_c W[c][p] T_d[p][c] on the vector pipe, reduced over
+//            the 4 lanes of a fragment row and over the warps in shared memory.
+//
+// Fragment layouts of m8n8k4.f64 (lane l, g = l >> 2, t = l & 3):
+//   A (8x4, row): A[g][t];  B (4x8, col): B[t][g];  C (8x8): C[g][2t], C[g][2t+1].
 #include "pif_internal.cuh"
 
 namespace pif {
 
-constexpr int kChunk = 64;  // particles staged per shared-memory round
+constexpr int kChunk = 64;  // particles staged per shared-memory round (multiple of 8)
 
-template <int R>
-struct TileSmem {
-  double psi[kChunk][3][R];
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int wrapi(int i, int n) { return ((i % n) + n) % n; }
+
+// psi_z row stride (doubles): == 8 words mod 32 so the 4 rows touched by one
+// half-warp fragment load fall in disjoint banks.
+template <int RZ>
+struct ZStride {
+  static constexpr int v = RZ == 16 ? 20 : (RZ == 8 ? 12 : RZ + 4);
+};
+
+template <int RX, int RY, int RZ>
+struct Psi {
+  double px[kChunk][RX];
+  double py[kChunk][RY];
+  double pz[kChunk][ZStride<RZ>::v];
   double xs[kChunk][3];
   int rel[kChunk][3];
   double str[kChunk];
 };
 
-template <int R>
-__device__ __forceinline__ void brick_origin(const Brick& g, int brick, int T0[3]) {
-  int bz = brick % g.nb, by = (brick / g.nb) % g.nb, bx = brick / (g.nb * g.nb);
-  T0[0] = bx * g.b - g.hw;
-  T0[1] = by * g.b - g.hw;
-  T0[2] = bz * g.b - g.hw;
+// Decode a spread brick (sub == false) or interpolation sub-brick (sub == true)
+// from the CTA index into its tile origin T0 (grid points) and particle range.
+__device__ __forceinline__ void tile_of(const Brick& g, int cta, bool sub, int T0[3],
+                                        const int* __restrict__ offsets, int64_t& start,
+                                        int64_t& end) {
+  const int M = g.m[0] * g.m[1] * g.m[2];
+  int brick = sub ? cta / M : cta;
+  int bz = brick % g.NB[2], by = (brick / g.NB[2]) % g.NB[1], bx = brick / (g.NB[2] * g.NB[1]);
+  T0[0] = bx * g.sb[0] - g.hw;
+  T0[1] = by * g.sb[1] - g.hw;
+  T0[2] = bz * g.sb[2] - g.hw;
+  if (sub) {
+    int s = cta % M;
+    int sz = s % g.m[2], sy = (s / g.m[2]) % g.m[1], sx = s / (g.m[2] * g.m[1]);
+    T0[0] += sx * g.ib[0];
+    T0[1] += sy * g.ib[1];
+    T0[2] += sz * g.ib[2];
+    start = offsets[cta];
+    end = offsets[cta + 1];
+  } else {
+    start = offsets[brick * M];
+    end = offsets[(brick + 1) * M];
+  }
 }
 
-// Stage positions and ES weights of particles [base, base+cnt) of the sorted
-// arrays into shared memory.  Ends with __syncthreads().
-template <int R, bool HAS_S>
-__device__ __forceinline__ void stage_chunk(TileSmem<R>& sm, const double* __restrict__ x,
-                                            int64_t stride, const double* __restrict__ s,
-                                            int64_t base, int cnt, const Brick& g,
-                                            const int T0[3]) {
-  const int tid = threadIdx.x;
-  if (tid < cnt) {
+// Thread tid < cnt: record particle tid's grid coordinate and window offset.
+template <int RX, int RY, int RZ>
+__device__ __forceinline__ void stage_position(Psi<RX, RY, RZ>& sm, int tid, const double xr[3],
+                                               const Brick& g, const int T0[3]) {
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      double xs = x[d * stride + base + tid] * g.scale;
-      int a = anchor_of(xs, g);
-      sm.xs[tid][d] = xs;
-      sm.rel[tid][d] = a - g.hw - T0[d];
-    }
-    if (HAS_S) sm.str[tid] = s[base + tid];
+  for (int d = 0; d < 3; ++d) {
+    double xs = xr[d] * g.scale;
+    int a = anchor_of(xs, g);
+    sm.xs[tid][d] = xs;
+    sm.rel[tid][d] = a - g.hw - T0[d];
   }
+}
+
+// ES weights of the chunk's particles (positions already staged); particles
+// cnt .. pad-1 get zero weights.  Starts and ends with __syncthreads().
+template <int RX, int RY, int RZ>
+__device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ>& sm, int cnt, int pad, const Brick& g,
+                                          const int T0[3]) {
   __syncthreads();
   const double two_over_w = 2.0 / g.w;
-  for (int it = tid; it < cnt * 3 * R; it += blockDim.x) {
-    int p = it / (3 * R);
-    int rem = it - p * 3 * R;
-    int d = rem / R;
-    int t = rem - d * R;
-    int r = t - sm.rel[p][d];
+  constexpr int RT = RX + RY + RZ;
+  for (int it = threadIdx.x; it < pad * RT; it += blockDim.x) {
+    int p = it / RT;
+    int t = it - p * RT;
+    int d = t < RX ? 0 : (t < RX + RY ? 1 : 2);
+    int u = d == 0 ? t : (d == 1 ? t - RX : t - RX - RY);
     double val = 0.0;
-    if (r >= 0 && r < g.w) val = es_kernel((double)(T0[d] + t) - sm.xs[p][d], two_over_w, g.beta);
-    sm.psi[p][d][t] = val;
+    if (p < cnt) {
+      int r = u - sm.rel[p][d];
+      if (r >= 0 && r < g.w)
+        val = es_kernel((double)((d == 0 ? T0[0] : d == 1 ? T0[1] : T0[2]) + u) - sm.xs[p][d],
+                        two_over_w, g.beta);
+    }
+    if (d == 0) sm.px[p][u] = val;
+    else if (d == 1) sm.py[p][u] = val;
+    else sm.pz[p][u] = val;
   }
   __syncthreads();
 }
 
-template <int R, bool HAS_S>
-__global__ void __launch_bounds__(((R * R + 31) / 32) * 32)
+// ------------------------------------------------------------------ spread --
+template <int RX, int RY, int RZ>
+struct SpreadCfg {
+  static constexpr int CT = 4;                    // column tiles (of 8) per warp
+  static constexpr int NW = RX * RY / (8 * CT);   // warps
+  static constexpr int ZT = RZ / 8;               // z tiles (of 8)
+  static_assert(RX * RY % (8 * CT) == 0 && RZ % 8 == 0, "tile shape");
+};
+
+template <int RX, int RY, int RZ, bool HAS_S>
+__global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
     k_spread(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
              double s_uniform, const int* __restrict__ offsets, Brick g, double* __restrict__ grid) {
-  __shared__ TileSmem<R> sm;
-  const int brick = blockIdx.x;
-  const int64_t start = offsets[brick], end = offsets[brick + 1];
-  if (start == end) return;
+  using C = SpreadCfg<RX, RY, RZ>;
+  __shared__ Psi<RX, RY, RZ> sm;
   int T0[3];
-  brick_origin<R>(g, brick, T0);
-  const int tid = threadIdx.x;
-  const bool col = tid < R * R;
-  const int tx = col ? tid % R : 0, ty = col ? tid / R : 0;
-  double acc[R];
+  int64_t start, end;
+  tile_of(g, blockIdx.x, false, T0, offsets, start, end);
+  if (start == end) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int gr = lane >> 2, tq = lane & 3;
+  // A-fragment rows: column c = (wid*CT + ct)*8 + gr
+  int acx[C::CT], acy[C::CT];
 #pragma unroll
-  for (int z = 0; z < R; ++z) acc[z] = 0.0;
+  for (int ct = 0; ct < C::CT; ++ct) {
+    int c = (wid * C::CT + ct) * 8 + gr;
+    acx[ct] = c % RX;
+    acy[ct] = c / RX;
+  }
+  double acc[C::CT][C::ZT][2];
+#pragma unroll
+  for (int ct = 0; ct < C::CT; ++ct)
+#pragma unroll
+    for (int zt = 0; zt < C::ZT; ++zt) acc[ct][zt][0] = acc[ct][zt][1] = 0.0;
 
   for (int64_t base = start; base < end; base += kChunk) {
     const int cnt = (int)min((int64_t)kChunk, end - base);
-    stage_chunk<R, HAS_S>(sm, x, stride, s, base, cnt, g, T0);
-    if (col) {
-      for (int p = 0; p < cnt; ++p) {
-        double c = sm.psi[p][0][tx] * sm.psi[p][1][ty];
-        if (HAS_S) c *= sm.str[p];
+    const int pad = (cnt + 3) & ~3;
+    if (tid < cnt) {
+      double xr[3] = {x[base + tid], x[stride + base + tid], x[2 * stride + base + tid]};
+      stage_position(sm, tid, xr, g, T0);
+      if (HAS_S) sm.str[tid] = s[base + tid];
+    }
+    stage_psi(sm, cnt, pad, g, T0);
+    for (int p0 = 0; p0 < pad; p0 += 4) {
+      const int pl = p0 + tq;  // K index of this lane's A and B elements
+      double b[C::ZT];
 #pragma unroll
-        for (int z = 0; z < R; ++z) acc[z] = fma(c, sm.psi[p][2][z], acc[z]);
+      for (int zt = 0; zt < C::ZT; ++zt) b[zt] = sm.pz[pl][zt * 8 + gr];
+      double sp = 1.0;
+      if (HAS_S) sp = pl < cnt ? sm.str[pl] : 0.0;
+#pragma unroll
+      for (int ct = 0; ct < C::CT; ++ct) {
+        double a = sm.px[pl][acx[ct]] * sm.py[pl][acy[ct]];
+        if (HAS_S) a *= sp;
+#pragma unroll
+        for (int zt = 0; zt < C::ZT; ++zt) dmma(acc[ct][zt], a, b[zt]);
       }
     }
     __syncthreads();
   }
-  if (!col) return;
+  // flush: C[g][2t+i] = G[column (wid*CT+ct)*8 + gr][z = zt*8 + 2t + i]
   const int n = g.n;
-  const int gx = ((T0[0] + tx) % n + n) % n;
-  const int gy = ((T0[1] + ty) % n + n) % n;
-  double* colp = grid + ((int64_t)gx * n + gy) * n;
 #pragma unroll
-  for (int z = 0; z < R; ++z) {
-    if (acc[z] != 0.0) {
-      int gz = ((T0[2] + z) % n + n) % n;
-      atomicAdd(colp + gz, acc[z] * s_uniform);
-    }
+  for (int ct = 0; ct < C::CT; ++ct) {
+    double* colp = grid + ((int64_t)wrapi(T0[0] + acx[ct], n) * n + wrapi(T0[1] + acy[ct], n)) * n;
+#pragma unroll
+    for (int zt = 0; zt < C::ZT; ++zt)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double val = acc[ct][zt][i];
+        if (val != 0.0) atomicAdd(colp + wrapi(T0[2] + zt * 8 + 2 * tq + i, n), val * s_uniform);
+      }
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(((R * R + 31) / 32) * 32, 1)
+// ------------------------------------------------------------ interp+push --
+template <int RX, int RY, int RZ>
+struct InterpCfg {
+  static constexpr int CT = 2;                    // column tiles (of 8) per warp
+  static constexpr int NW = RX * RY / (8 * CT);   // warps
+  static constexpr int KS = RZ / 4;               // k steps (z) per MMA chain
+  static_assert(RX * RY % (8 * CT) == 0 && RZ % 4 == 0, "tile shape");
+};
+
+template <int RX, int RY, int RZ>
+struct InterpSmem {
+  Psi<RX, RY, RZ> psi;
+  double red[kChunk][InterpCfg<RX, RY, RZ>::NW][3];
+};
+
+template <int RX, int RY, int RZ>
+__global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
     k_interp_push(const double* __restrict__ grid3, double* __restrict__ x,
                   double* __restrict__ v, int64_t stride, const int* __restrict__ id,
                   double* __restrict__ Eout, const int* __restrict__ offsets, Brick g, PushArgs P) {
-  constexpr int NW = ((R * R + 31) / 32);
-  __shared__ TileSmem<R> sm;
-  __shared__ double red[kChunk][NW][3];
-  const int brick = blockIdx.x;
-  const int64_t start = offsets[brick], end = offsets[brick + 1];
-  if (start == end) return;
+  using C = InterpCfg<RX, RY, RZ>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  InterpSmem<RX, RY, RZ>& S = *reinterpret_cast<InterpSmem<RX, RY, RZ>*>(smem_raw);
+  Psi<RX, RY, RZ>& sm = S.psi;
   int T0[3];
-  brick_origin<R>(g, brick, T0);
+  int64_t start, end;
+  tile_of(g, blockIdx.x, true, T0, offsets, start, end);
+  if (start == end) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool col = tid < R * R;
-  const int tx = col ? tid % R : 0, ty = col ? tid / R : 0;
+  const int gr = lane >> 2, tq = lane & 3;
   const int n = g.n;
   const int64_t n3 = (int64_t)n * n * n;
-  double g0[R], g1[R], g2[R];
-  {
-    const int gx = ((T0[0] + tx) % n + n) % n;
-    const int gy = ((T0[1] + ty) % n + n) % n;
-    const int64_t cb = ((int64_t)gx * n + gy) * n;
+  // B fragments: B[k = tq][col = gr] = g_d[z = ks*4 + tq][c = (wid*CT+ct)*8 + gr]
+  double gb[C::CT][C::KS][3];
 #pragma unroll
-    for (int z = 0; z < R; ++z) {
-      int gz = ((T0[2] + z) % n + n) % n;
-      g0[z] = col ? grid3[cb + gz] : 0.0;
-      g1[z] = col ? grid3[n3 + cb + gz] : 0.0;
-      g2[z] = col ? grid3[2 * n3 + cb + gz] : 0.0;
+  for (int ct = 0; ct < C::CT; ++ct) {
+    int c = (wid * C::CT + ct) * 8 + gr;
+    const int64_t cb = ((int64_t)wrapi(T0[0] + c % RX, n) * n + wrapi(T0[1] + c / RX, n)) * n;
+#pragma unroll
+    for (int ks = 0; ks < C::KS; ++ks) {
+      int gz = wrapi(T0[2] + ks * 4 + tq, n);
+      gb[ct][ks][0] = grid3[cb + gz];
+      gb[ct][ks][1] = grid3[n3 + cb + gz];
+      gb[ct][ks][2] = grid3[2 * n3 + cb + gz];
     }
   }
+  // C-fragment columns of this lane: c = (wid*CT+ct)*8 + 2*tq + i
+  int ccx[C::CT][2], ccy[C::CT][2];
+#pragma unroll
+  for (int ct = 0; ct < C::CT; ++ct)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      int c = (wid * C::CT + ct) * 8 + 2 * tq + i;
+      ccx[ct][i] = c % RX;
+      ccy[ct][i] = c / RX;
+    }
+
   for (int64_t base = start; base < end; base += kChunk) {
     const int cnt = (int)min((int64_t)kChunk, end - base);
-    stage_chunk<R, false>(sm, x, stride, nullptr, base, cnt, g, T0);
-    for (int p = 0; p < cnt; ++p) {
-      double c = sm.psi[p][0][tx] * sm.psi[p][1][ty];
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int z = 0; z < R; ++z) {
-        double pz = sm.psi[p][2][z];
-        s0 = fma(pz, g0[z], s0);
-        s1 = fma(pz, g1[z], s1);
-        s2 = fma(pz, g2[z], s2);
+    const int pad = (cnt + 7) & ~7;
+    double xr[3] = {0, 0, 0}, vr[3] = {0, 0, 0};
+    if (tid < cnt) {
+      const int64_t j = base + tid;
+      xr[0] = x[j];
+      xr[1] = x[stride + j];
+      xr[2] = x[2 * stride + j];
+      if (v) {
+        vr[0] = v[j];
+        vr[1] = v[stride + j];
+        vr[2] = v[2 * stride + j];
       }
-      s0 *= c;
-      s1 *= c;
-      s2 *= c;
+      stage_position(sm, tid, xr, g, T0);
+    }
+    stage_psi(sm, cnt, pad, g, T0);
+    for (int p0 = 0; p0 < pad; p0 += 8) {
+      double acc[C::CT][3][2];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      for (int ct = 0; ct < C::CT; ++ct)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) acc[ct][d][0] = acc[ct][d][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < C::KS; ++ks) {
+        const double a = sm.pz[p0 + gr][ks * 4 + tq];  // A[g][t] = psi_z[p0+g][z]
+#pragma unroll
+        for (int ct = 0; ct < C::CT; ++ct)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) dmma(acc[ct][d], a, gb[ct][ks][d]);
       }
-      if (lane == 0) {
-        red[p][wid][0] = s0;
-        red[p][wid][1] = s1;
-        red[p][wid][2] = s2;
+      const int p = p0 + gr;
+      double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+#pragma unroll
+      for (int ct = 0; ct < C::CT; ++ct)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double W = sm.px[p][ccx[ct][i]] * sm.py[p][ccy[ct][i]];
+          e0 = fma(W, acc[ct][0][i], e0);
+          e1 = fma(W, acc[ct][1][i], e1);
+          e2 = fma(W, acc[ct][2][i], e2);
+        }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        e0 += __shfl_xor_sync(0xffffffffu, e0, o);
+        e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+      }
+      if (tq == 0) {
+        S.red[p][wid][0] = e0;
+        S.red[p][wid][1] = e1;
+        S.red[p][wid][2] = e2;
       }
     }
     __syncthreads();
     if (tid < cnt) {
       double E0 = 0.0, E1 = 0.0, E2 = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        E0 += red[tid][w][0];
-        E1 += red[tid][w][1];
-        E2 += red[tid][w][2];
+      for (int w = 0; w < C::NW; ++w) {
+        E0 += S.red[tid][w][0];
+        E1 += S.red[tid][w][1];
+        E2 += S.red[tid][w][2];
       }
       const int64_t j = base + tid;
       if (Eout) {
@@ -187,54 +325,67 @@ __global__ void __launch_bounds__(((R * R + 31) / 32) * 32, 1)
         Eout[2 * stride + k] = E2;
       }
       if (P.kicks > 0 || P.drift) {
-        double x0 = x[j], x1 = x[stride + j], x2 = x[2 * stride + j];
-        double v0 = v[j], v1 = v[stride + j], v2 = v[2 * stride + j];
-        push_particle(x0, x1, x2, v0, v1, v2, E0, E1, E2, P);
-        x[j] = x0;
-        x[stride + j] = x1;
-        x[2 * stride + j] = x2;
-        v[j] = v0;
-        v[stride + j] = v1;
-        v[2 * stride + j] = v2;
+        push_particle(xr[0], xr[1], xr[2], vr[0], vr[1], vr[2], E0, E1, E2, P);
+        x[j] = xr[0];
+        x[stride + j] = xr[1];
+        x[2 * stride + j] = xr[2];
+        v[j] = vr[0];
+        v[stride + j] = vr[1];
+        v[2 * stride + j] = vr[2];
       }
     }
     __syncthreads();
   }
 }
 
-static int tile_threads(int R) { return ((R * R + 31) / 32) * 32; }
-
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
                           const int* offsets, const Brick& g, double* grid, cudaStream_t st) {
-  const unsigned nbr = (unsigned)((int64_t)g.nb * g.nb * g.nb);
-  const int T = tile_threads(g.R);
-#define PIF_SPREAD(RR)                                                                        \
-  if (s)                                                                                      \
-    k_spread<RR, true><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, grid);         \
-  else                                                                                        \
-    k_spread<RR, false><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, grid);
-  switch (g.R) {
-    case 8: PIF_SPREAD(8) break;
-    case 12: PIF_SPREAD(12) break;
-    case 16: PIF_SPREAD(16) break;
-    default: return cudaErrorInvalidValue;
+  const unsigned nbr = (unsigned)((int64_t)g.NB[0] * g.NB[1] * g.NB[2]);
+#define PIF_SPREAD(A, B, Cz)                                                                  \
+  if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz) {                                        \
+    const int T = 32 * SpreadCfg<A, B, Cz>::NW;                                               \
+    if (s)                                                                                    \
+      k_spread<A, B, Cz, true><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, grid); \
+    else                                                                                      \
+      k_spread<A, B, Cz, false><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, grid); \
+    return cudaGetLastError();                                                                \
   }
+  PIF_SPREAD(8, 8, 8)
+  PIF_SPREAD(16, 14, 16)
+  PIF_SPREAD(16, 16, 16)
 #undef PIF_SPREAD
+  return cudaErrorInvalidValue;
+}
+
+template <int A, int B, int Cz>
+static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, double* v,
+                                 int64_t stride, const int* id, double* Eout, const int* offsets,
+                                 const Brick& g, const PushArgs& P, cudaStream_t st) {
+  const int T = 32 * InterpCfg<A, B, Cz>::NW;
+  const size_t smem = sizeof(InterpSmem<A, B, Cz>);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_interp_push<A, B, Cz>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_interp_push<A, B, Cz><<<nsub, T, smem, st>>>(grid3, x, v, stride, id, Eout, offsets, g, P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
                                const int* id, double* Eout, const int* offsets, const Brick& g,
                                const PushArgs& P, cudaStream_t st) {
-  const unsigned nbr = (unsigned)((int64_t)g.nb * g.nb * g.nb);
-  const int T = tile_threads(g.R);
-  switch (g.R) {
-    case 8: k_interp_push<8><<<nbr, T, 0, st>>>(grid3, x, v, stride, id, Eout, offsets, g, P); break;
-    case 12: k_interp_push<12><<<nbr, T, 0, st>>>(grid3, x, v, stride, id, Eout, offsets, g, P); break;
-    case 16: k_interp_push<16><<<nbr, T, 0, st>>>(grid3, x, v, stride, id, Eout, offsets, g, P); break;
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+  const unsigned nsub = (unsigned)g.nkeys;
+#define PIF_INTERP(A, B, Cz)                                                                   \
+  if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
+    return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, P, st);
+  PIF_INTERP(8, 8, 8)
+  PIF_INTERP(16, 14, 16)
+  PIF_INTERP(16, 16, 16)
+#undef PIF_INTERP
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace pif
