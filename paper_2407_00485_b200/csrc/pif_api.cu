@@ -112,8 +112,51 @@ enum { PH_SORT = 0, PH_SPREAD, PH_FFT_FWD, PH_BOX, PH_ALLREDUCE, PH_POISSON, PH_
        PH_INTERP_PUSH, PH_PIC_DEPOSIT, PH_PIC_GATHER_PUSH, PH_OTHER, PH_COUNT };
 static_assert(PH_COUNT == PIF_NPHASES, "phase count");
 
+// Chebyshev interpolation of psi(k - hw - f) on f in [f_lo, f_lo + 1) at
+// kHornerDeg + 1 Chebyshev nodes of s = 2 (f - f_lo) - 1, converted to monomial
+// coefficients in s (three-term recurrence of T_j).
+void horner_fit(int w, double beta, Horner& hc) {
+  const int D = kHornerDeg, hw = (w - 1) / 2;
+  const double flo = (w & 1) ? -0.5 : 0.0;
+  memset(&hc, 0, sizeof(hc));
+  std::vector<double> sn(D + 1), cheb(D + 1);
+  for (int i = 0; i <= D; ++i) sn[i] = std::cos(M_PI * (i + 0.5) / (D + 1));
+  for (int k = 0; k < w; ++k) {
+    std::vector<double> val(D + 1);
+    for (int i = 0; i <= D; ++i) {
+      double f = flo + 0.5 * (sn[i] + 1.0);
+      val[i] = es_host(k - hw - f, w, beta);
+    }
+    for (int j = 0; j <= D; ++j) {
+      double acc = 0;
+      for (int i = 0; i <= D; ++i) acc += val[i] * std::cos(M_PI * j * (i + 0.5) / (D + 1));
+      cheb[j] = acc * (j == 0 ? 1.0 : 2.0) / (D + 1);
+    }
+    // monomial coefficients: sum_j cheb[j] T_j(s)
+    std::vector<double> Tm1(D + 1, 0.0), T0(D + 1, 0.0), T1(D + 1, 0.0), mono(D + 1, 0.0);
+    T0[0] = 1.0;  // T_0
+    for (int j = 0; j <= D; ++j) {
+      const std::vector<double>& Tj = (j == 0) ? T0 : T1;
+      for (int q = 0; q <= D; ++q) mono[q] += cheb[j] * Tj[q];
+      // advance: T_{j+1} = 2 s T_j - T_{j-1}
+      std::vector<double> nxt(D + 1, 0.0);
+      if (j == 0) {
+        nxt[1] = 1.0;  // T_1 = s
+        Tm1 = T0;
+      } else {
+        for (int q = 0; q < D; ++q) nxt[q + 1] += 2.0 * T1[q];
+        for (int q = 0; q <= D; ++q) nxt[q] -= Tm1[q];
+        Tm1 = T1;
+      }
+      T1 = nxt;
+    }
+    for (int q = 0; q <= D; ++q) hc.a[k][q] = mono[q];
+  }
+}
+
 struct Plan {
   bool valid = false;
+  Horner hc{};
   int kind = 0, N = 0, order = 1;
   double tol = 0, dt = 0;
   Brick g{};
@@ -248,6 +291,7 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     }
     g.scale = n / L;
     g.beta = es_beta(w);
+    horner_fit(w, g.beta, p.hc);
     p.n = n;
     p.nbricks = g.nkeys;
     c->max_bins = std::max(c->max_bins, p.nbricks);
@@ -374,7 +418,7 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_SORT, TRY(sort_particles(c, p)));
     PH(PH_SPREAD, {
       CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-      CU(launch_spread(c->xA, n, nullptr, 1.0, c->offsets, p.g, p.grid, c->st));
+      CU(launch_spread(c->xA, n, nullptr, 1.0, c->offsets, p.g, p.hc, p.grid, c->st));
     });
     PH(PH_FFT_FWD, CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec)));
     const double L = c->ph.L;
@@ -385,7 +429,7 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_POISSON, CU(launch_poisson_pad(p.box, p.n, p.N, L, p.cor, p.S, p.G3, c->st)));
     PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
     PH(PH_INTERP_PUSH, CU(launch_interp_push(p.grid3, c->xA, c->vA, n, c->idA, nullptr,
-                                             c->offsets, p.g, P, c->st)));
+                                             c->offsets, p.g, p.hc, P, c->st)));
     c->launches += 7;  // bin, scan, scatter, spread, extract, poisson, interp_push
     c->box_fresh = (which == 0) && !drift;
   } else {
@@ -970,7 +1014,7 @@ pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, con
   CU(launch_scan(counts, offs, p.nbricks, c->st));
   CU(launch_scatter_sorted(dx, nullptr, id, ds, n, n, key, rk, offs, dx2, nullptr, id2, ds2, c->st));
   CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-  CU(launch_spread(dx2, n, ds2, 1.0, offs, p.g, p.grid, c->st));
+  CU(launch_spread(dx2, n, ds2, 1.0, offs, p.g, p.hc, p.grid, c->st));
   CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec));
   CU(launch_debug_extract_KN(p.spec, p.n, p.N, p.cor, dout, c->st));
   CU(cudaMemcpyAsync(out, dout, N3 * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
@@ -1010,7 +1054,7 @@ pif_status pif_debug_type2(pif_ctx c, int which, const double* cin, const double
   CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, c->st));
   CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3));
   PushArgs P = push_args(c, p, 0, 0);
-  CU(launch_interp_push(p.grid3, dx2, nullptr, n, id2, E, offs, p.g, P, c->st));
+  CU(launch_interp_push(p.grid3, dx2, nullptr, n, id2, E, offs, p.g, p.hc, P, c->st));
   CU(cudaMemcpyAsync(out, E, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CU(cudaStreamSynchronize(c->st));
   cudaFree(dx); cudaFree(dx2); cudaFree(E); cudaFree(id); cudaFree(counts); cudaFree(dc);

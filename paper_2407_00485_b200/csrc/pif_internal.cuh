@@ -45,6 +45,19 @@ struct Brick {
   double beta;   // ES shape parameter
 };
 
+// Piecewise-polynomial ES kernel: for a particle
+// with fractional offset f = x~ - a (f in [-1/2, 1/2) for odd w, [0, 1) for even
+// w) the window node k (grid point a - hw + k) has weight psi(k - hw - f) =
+// P_k(s), s = 2 (f - f_lo) - 1 in [-1, 1], with P_k a degree-kHornerDeg
+// Chebyshev interpolant in monomial form (max error ~5e-15 on interior nodes).
+// The two edge nodes k = 0, w-1 carry the sqrt singularity of psi at |t| = w/2
+// and are evaluated exactly.  Passed by value as a __grid_constant__ kernel
+// parameter: every lane of a warp reads the same coefficient (constant cache).
+constexpr int kHornerDeg = 14;
+struct Horner {
+  double a[16][kHornerDeg + 1];  // a[k][j]: coefficient of s^j for node k
+};
+
 // Anchor cell of coordinate xs (grid units) with the window rule above; xs is
 // shifted by -n / +n when the anchor wraps so that g - xs stays the true offset.
 __device__ __forceinline__ int anchor_of(double& xs, const Brick& g) {
@@ -128,10 +141,11 @@ cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* i
                                   const int* offsets, double* x2, double* v2, int* id2, double* s2,
                                   cudaStream_t st);
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const int* offsets, const Brick& g, double* grid, cudaStream_t st);
+                          const int* offsets, const Brick& g, const Horner& hc, double* grid,
+                          cudaStream_t st);
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
                                const int* id, double* Eout, const int* offsets, const Brick& g,
-                               const PushArgs& P, cudaStream_t st);
+                               const Horner& hc, const PushArgs& P, cudaStream_t st);
 cudaError_t launch_extract_box(const double2* spec, int n, int N, const double* cor, double scale,
                                double2* box, cudaStream_t st);
 cudaError_t launch_poisson_pad(const double2* box, int n, int N, double L, const double* cor,

@@ -39,18 +39,19 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 
 __device__ __forceinline__ int wrapi(int i, int n) { return ((i % n) + n) % n; }
 
-// psi_z row stride (doubles): == 8 words mod 32 so the 4 rows touched by one
-// half-warp fragment load fall in disjoint banks.
-template <int RZ>
-struct ZStride {
-  static constexpr int v = RZ == 16 ? 20 : (RZ == 8 ? 12 : RZ + 4);
+// psi row strides (doubles): S == 4 or 12 (mod 16) so that the 4 particle rows
+// read by one half-warp fragment load (4 consecutive doubles each) fall in
+// disjoint banks.
+template <int R>
+struct RowStride {
+  static constexpr int v = R <= 8 ? 12 : (R <= 16 ? 20 : ((R + 11) / 16) * 16 + 4);
 };
 
 template <int RX, int RY, int RZ>
 struct Psi {
-  double px[kChunk][RX];
-  double py[kChunk][RY];
-  double pz[kChunk][ZStride<RZ>::v];
+  double px[kChunk][RowStride<RX>::v];
+  double py[kChunk][RowStride<RY>::v];
+  double pz[kChunk][RowStride<RZ>::v];
   double xs[kChunk][3];
   int rel[kChunk][3];
   double str[kChunk];
@@ -95,28 +96,38 @@ __device__ __forceinline__ void stage_position(Psi<RX, RY, RZ>& sm, int tid, con
 }
 
 // ES weights of the chunk's particles (positions already staged); particles
-// cnt .. pad-1 get zero weights.  Starts and ends with __syncthreads().
+// cnt .. pad-1 get zero rows.  One item per (dimension, particle): the w window
+// weights by per-node Horner polynomials (edge nodes exactly), zeros elsewhere
+// in the tile row.  Starts and ends with __syncthreads().
 template <int RX, int RY, int RZ>
 __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ>& sm, int cnt, int pad, const Brick& g,
-                                          const int T0[3]) {
+                                          const int T0[3], const Horner& hc) {
   __syncthreads();
   const double two_over_w = 2.0 / g.w;
-  constexpr int RT = RX + RY + RZ;
-  for (int it = threadIdx.x; it < pad * RT; it += blockDim.x) {
-    int p = it / RT;
-    int t = it - p * RT;
-    int d = t < RX ? 0 : (t < RX + RY ? 1 : 2);
-    int u = d == 0 ? t : (d == 1 ? t - RX : t - RX - RY);
-    double val = 0.0;
-    if (p < cnt) {
-      int r = u - sm.rel[p][d];
-      if (r >= 0 && r < g.w)
-        val = es_kernel((double)((d == 0 ? T0[0] : d == 1 ? T0[1] : T0[2]) + u) - sm.xs[p][d],
-                        two_over_w, g.beta);
+  const double flo = g.odd ? -0.5 : 0.0;
+  const int w = g.w;
+  for (int it = threadIdx.x; it < 3 * pad; it += blockDim.x) {
+    const int d = it / pad, p = it - d * pad;
+    const int R = d == 0 ? RX : (d == 1 ? RY : RZ);
+    double* row = d == 0 ? sm.px[p] : (d == 1 ? sm.py[p] : sm.pz[p]);
+    if (p >= cnt) {
+      for (int u = 0; u < R; ++u) row[u] = 0.0;
+      continue;
     }
-    if (d == 0) sm.px[p][u] = val;
-    else if (d == 1) sm.py[p][u] = val;
-    else sm.pz[p][u] = val;
+    const int rel = sm.rel[p][d];
+    const int T0d = d == 0 ? T0[0] : (d == 1 ? T0[1] : T0[2]);
+    const double f = sm.xs[p][d] - (double)(rel + g.hw + T0d);  // x~ - anchor
+    const double sv = 2.0 * (f - flo) - 1.0;
+    for (int u = 0; u < rel; ++u) row[u] = 0.0;
+    for (int u = rel + w; u < R; ++u) row[u] = 0.0;
+    row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
+    row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+    for (int k = 1; k < w - 1; ++k) {
+      double acc = hc.a[k][kHornerDeg];
+#pragma unroll
+      for (int j = kHornerDeg - 1; j >= 0; --j) acc = fma(acc, sv, hc.a[k][j]);
+      row[rel + k] = acc;
+    }
   }
   __syncthreads();
 }
@@ -133,7 +144,8 @@ struct SpreadCfg {
 template <int RX, int RY, int RZ, bool HAS_S>
 __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
     k_spread(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
-             double s_uniform, const int* __restrict__ offsets, Brick g, double* __restrict__ grid) {
+             double s_uniform, const int* __restrict__ offsets, Brick g,
+             const __grid_constant__ Horner hc, double* __restrict__ grid) {
   using C = SpreadCfg<RX, RY, RZ>;
   __shared__ Psi<RX, RY, RZ> sm;
   int T0[3];
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
       stage_position(sm, tid, xr, g, T0);
       if (HAS_S) sm.str[tid] = s[base + tid];
     }
-    stage_psi(sm, cnt, pad, g, T0);
+    stage_psi(sm, cnt, pad, g, T0, hc);
     for (int p0 = 0; p0 < pad; p0 += 4) {
       const int pl = p0 + tq;  // K index of this lane's A and B elements
       double b[C::ZT];
@@ -216,7 +228,8 @@ template <int RX, int RY, int RZ>
 __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
     k_interp_push(const double* __restrict__ grid3, double* __restrict__ x,
                   double* __restrict__ v, int64_t stride, const int* __restrict__ id,
-                  double* __restrict__ Eout, const int* __restrict__ offsets, Brick g, PushArgs P) {
+                  double* __restrict__ Eout, const int* __restrict__ offsets, Brick g,
+                  const __grid_constant__ Horner hc, PushArgs P) {
   using C = InterpCfg<RX, RY, RZ>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   InterpSmem<RX, RY, RZ>& S = *reinterpret_cast<InterpSmem<RX, RY, RZ>*>(smem_raw);
@@ -254,23 +267,29 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
       ccy[ct][i] = c / RX;
     }
 
+  // x, v of the next chunk are prefetched into registers during the MMA phase
+  double xn[3] = {0, 0, 0}, vn[3] = {0, 0, 0};
+  auto fetch = [&](int64_t b, int c) {
+    if (tid < c) {
+      const int64_t j = b + tid;
+      xn[0] = x[j];
+      xn[1] = x[stride + j];
+      xn[2] = x[2 * stride + j];
+      if (v) {
+        vn[0] = v[j];
+        vn[1] = v[stride + j];
+        vn[2] = v[2 * stride + j];
+      }
+    }
+  };
+  fetch(start, (int)min((int64_t)kChunk, end - start));
   for (int64_t base = start; base < end; base += kChunk) {
     const int cnt = (int)min((int64_t)kChunk, end - base);
     const int pad = (cnt + 7) & ~7;
-    double xr[3] = {0, 0, 0}, vr[3] = {0, 0, 0};
-    if (tid < cnt) {
-      const int64_t j = base + tid;
-      xr[0] = x[j];
-      xr[1] = x[stride + j];
-      xr[2] = x[2 * stride + j];
-      if (v) {
-        vr[0] = v[j];
-        vr[1] = v[stride + j];
-        vr[2] = v[2 * stride + j];
-      }
-      stage_position(sm, tid, xr, g, T0);
-    }
-    stage_psi(sm, cnt, pad, g, T0);
+    double xr[3] = {xn[0], xn[1], xn[2]}, vr[3] = {vn[0], vn[1], vn[2]};
+    if (tid < cnt) stage_position(sm, tid, xr, g, T0);
+    stage_psi(sm, cnt, pad, g, T0, hc);
+    if (base + kChunk < end) fetch(base + kChunk, (int)min((int64_t)kChunk, end - base - kChunk));
     for (int p0 = 0; p0 < pad; p0 += 8) {
       double acc[C::CT][3][2];
 #pragma unroll
@@ -339,15 +358,16 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
 }
 
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const int* offsets, const Brick& g, double* grid, cudaStream_t st) {
+                          const int* offsets, const Brick& g, const Horner& hc, double* grid,
+                          cudaStream_t st) {
   const unsigned nbr = (unsigned)((int64_t)g.NB[0] * g.NB[1] * g.NB[2]);
 #define PIF_SPREAD(A, B, Cz)                                                                  \
   if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz) {                                        \
     const int T = 32 * SpreadCfg<A, B, Cz>::NW;                                               \
     if (s)                                                                                    \
-      k_spread<A, B, Cz, true><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, grid); \
+      k_spread<A, B, Cz, true><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid); \
     else                                                                                      \
-      k_spread<A, B, Cz, false><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, grid); \
+      k_spread<A, B, Cz, false><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid); \
     return cudaGetLastError();                                                                \
   }
   PIF_SPREAD(8, 8, 8)
@@ -360,7 +380,8 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
 template <int A, int B, int Cz>
 static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, double* v,
                                  int64_t stride, const int* id, double* Eout, const int* offsets,
-                                 const Brick& g, const PushArgs& P, cudaStream_t st) {
+                                 const Brick& g, const Horner& hc, const PushArgs& P,
+                                 cudaStream_t st) {
   const int T = 32 * InterpCfg<A, B, Cz>::NW;
   const size_t smem = sizeof(InterpSmem<A, B, Cz>);
   static bool attr = false;
@@ -370,17 +391,17 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_interp_push<A, B, Cz><<<nsub, T, smem, st>>>(grid3, x, v, stride, id, Eout, offsets, g, P);
+  k_interp_push<A, B, Cz><<<nsub, T, smem, st>>>(grid3, x, v, stride, id, Eout, offsets, g, hc, P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
                                const int* id, double* Eout, const int* offsets, const Brick& g,
-                               const PushArgs& P, cudaStream_t st) {
+                               const Horner& hc, const PushArgs& P, cudaStream_t st) {
   const unsigned nsub = (unsigned)g.nkeys;
 #define PIF_INTERP(A, B, Cz)                                                                   \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
-    return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, P, st);
+    return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
   PIF_INTERP(8, 8, 8)
   PIF_INTERP(16, 14, 16)
   PIF_INTERP(16, 16, 16)
