@@ -122,11 +122,18 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ>& sm, int cnt, int pad,
     for (int u = rel + w; u < R; ++u) row[u] = 0.0;
     row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
     row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
-    for (int k = 1; k < w - 1; ++k) {
-      double acc = hc.a[k][kHornerDeg];
+    // interior nodes 1 .. w-2, four independent Horner chains at a time
+    for (int k0 = 1; k0 < w - 1; k0 += 4) {
+      double acc[4];
 #pragma unroll
-      for (int j = kHornerDeg - 1; j >= 0; --j) acc = fma(acc, sv, hc.a[k][j]);
-      row[rel + k] = acc;
+      for (int q = 0; q < 4; ++q) acc[q] = hc.a[min(k0 + q, 15)][kHornerDeg];
+#pragma unroll
+      for (int j = kHornerDeg - 1; j >= 0; --j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(acc[q], sv, hc.a[min(k0 + q, 15)][j]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (k0 + q < w - 1) row[rel + k0 + q] = acc[q];
     }
   }
   __syncthreads();
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
 // ------------------------------------------------------------ interp+push --
 template <int RX, int RY, int RZ>
 struct InterpCfg {
-  static constexpr int CT = 2;                    // column tiles (of 8) per warp
+  static constexpr int CT = 4;                    // column tiles (of 8) per warp
   static constexpr int NW = RX * RY / (8 * CT);   // warps
   static constexpr int KS = RZ / 4;               // k steps (z) per MMA chain
   static_assert(RX * RY % (8 * CT) == 0 && RZ % 4 == 0, "tile shape");
@@ -290,8 +297,9 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
     if (tid < cnt) stage_position(sm, tid, xr, g, T0);
     stage_psi(sm, cnt, pad, g, T0, hc);
     if (base + kChunk < end) fetch(base + kChunk, (int)min((int64_t)kChunk, end - base - kChunk));
-    for (int p0 = 0; p0 < pad; p0 += 8) {
-      double acc[C::CT][3][2];
+    // Software-pipelined over m-tiles of 8 particles: the DMMAs of tile i+1 are
+    // issued before the vector-pipe stage 2 of tile i consumes its accumulators.
+    auto mma_tile = [&](int p0, double (&acc)[C::CT][3][2]) {
 #pragma unroll
       for (int ct = 0; ct < C::CT; ++ct)
 #pragma unroll
@@ -304,6 +312,8 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
 #pragma unroll
           for (int d = 0; d < 3; ++d) dmma(acc[ct][d], a, gb[ct][ks][d]);
       }
+    };
+    auto stage2 = [&](int p0, const double (&acc)[C::CT][3][2]) {
       const int p = p0 + gr;
       double e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
@@ -326,6 +336,18 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
         S.red[p][wid][1] = e1;
         S.red[p][wid][2] = e2;
       }
+    };
+    {
+      double accA[C::CT][3][2], accB[C::CT][3][2];
+      mma_tile(0, accA);
+      int p0 = 0;
+      for (; p0 + 16 <= pad; p0 += 16) {
+        mma_tile(p0 + 8, accB);
+        stage2(p0, accA);
+        if (p0 + 16 < pad) mma_tile(p0 + 16, accA);
+        stage2(p0 + 8, accB);
+      }
+      if (p0 < pad) stage2(p0, accA);  // pad % 16 == 8: last tile pending in accA
     }
     __syncthreads();
     if (tid < cnt) {
