@@ -187,6 +187,12 @@ struct pif_ctx_s {
   int device = 0, rank = 0, world = 1, space_size = 1, time_size = 1, s_idx = 0, t_idx = 0;
   cudaStream_t st = nullptr;
   ncclComm_t comm_world = nullptr, comm_space = nullptr, comm_time = nullptr;
+  // parareal hand-off t -> t+1 travels on comm_tp[t % 2]: a rank's sends and
+  // receives never share a communicator, so sends can run on st_comm while the
+  // next fine propagation runs on st.
+  ncclComm_t comm_tp[2] = {nullptr, nullptr};
+  cudaStream_t st_comm = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_sent = nullptr;
   // workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -592,9 +598,22 @@ pif_status pif_init(const pif_physics* phys, const pif_propagator* fine,
     // space group: same time index; time group: same space index.
     r = ncclCommSplit(c->comm_world, c->t_idx, c->s_idx, &c->comm_space, nullptr);
     if (r == ncclSuccess) r = ncclCommSplit(c->comm_world, c->s_idx, c->t_idx, &c->comm_time, nullptr);
+    if (r == ncclSuccess && c->time_size > 1) {
+      r = ncclCommSplit(c->comm_time, 0, c->t_idx, &c->comm_tp[0], nullptr);
+      if (r == ncclSuccess) r = ncclCommSplit(c->comm_time, 0, c->t_idx, &c->comm_tp[1], nullptr);
+    }
     if (r != ncclSuccess) {
       fail(PIF_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
       return bail(PIF_ERR_NCCL);
+    }
+  }
+  if (c->time_size > 1) {
+    e = cudaStreamCreateWithFlags(&c->st_comm, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_sent, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      fail(PIF_ERR_CUDA, std::string("comm stream: ") + cudaGetErrorString(e));
+      return bail(PIF_ERR_CUDA);
     }
   }
   *out = c;
@@ -843,14 +862,24 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
       free_all();
       return st;
     }
+    // send on the comm stream (ordered after the producer on st); any later
+    // write into a buffer waits for ev_sent (see guard()).
     auto nsend = [&](const double* buf) -> pif_status {
-      NC(ncclSend(buf, SZ, ncclDouble, t + 1, c->comm_time, c->st));
+      CU(cudaEventRecord(c->ev_ready, c->st));
+      CU(cudaStreamWaitEvent(c->st_comm, c->ev_ready, 0));
+      NC(ncclSend(buf, SZ, ncclDouble, t + 1, c->comm_tp[t % 2], c->st_comm));
+      CU(cudaEventRecord(c->ev_sent, c->st_comm));
       return PIF_OK;
     };
     auto nrecv = [&](double* buf) -> pif_status {
-      NC(ncclRecv(buf, SZ, ncclDouble, t - 1, c->comm_time, c->st));
+      NC(ncclRecv(buf, SZ, ncclDouble, t - 1, c->comm_tp[(t + 1) % 2], c->st));
       return PIF_OK;
     };
+    auto guard = [&]() -> pif_status {
+      CU(cudaStreamWaitEvent(c->st, c->ev_sent, 0));
+      return PIF_OK;
+    };
+    CU(cudaEventRecord(c->ev_sent, c->st));
     bool pred_retired = (t == 0), retired = false, changed = true;
     std::vector<double> myx(max_iter, NAN), myv(max_iter, NAN);
     int my_ret = -1;
@@ -875,6 +904,7 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
         changed = true;
       }
       double* Gn = Gold;
+      if ((st = guard()) != PIF_OK) break;
       if (changed) {
         st = timed(t_coarse, [&] { return propagate(1, U, Gnew); });
         if (st != PIF_OK) break;
@@ -895,6 +925,7 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
       CU(cudaMemcpyAsync(Unext + 6 * n, &fl, sizeof(double), cudaMemcpyHostToDevice, c->st));
       if (t + 1 < T) st = timed(t_comm, [&] { return nsend(Unext); });
     }
+    if (c->st_comm) cudaStreamSynchronize(c->st_comm);
     if (st == PIF_OK) st = load_state(c, Unext);
     // gather the report over the time group (small)
     if (st == PIF_OK && max_iter > 0) {
@@ -975,6 +1006,11 @@ pif_status pif_finalize(pif_ctx c) {
     if (c->plan[i].fwd) cufftDestroy(c->plan[i].fwd);
     if (c->plan[i].inv) cufftDestroy(c->plan[i].inv);
   }
+  for (int i = 0; i < 2; ++i)
+    if (c->comm_tp[i]) ncclCommDestroy(c->comm_tp[i]);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_sent) cudaEventDestroy(c->ev_sent);
+  if (c->st_comm) cudaStreamDestroy(c->st_comm);
   if (c->comm_space) ncclCommDestroy(c->comm_space);
   if (c->comm_time) ncclCommDestroy(c->comm_time);
   if (c->comm_world) ncclCommDestroy(c->comm_world);
