@@ -110,6 +110,11 @@ pif_status pif_init(const pif_physics* phys, const pif_propagator* fine,
    ranks one more). */
 pif_status pif_local_count(pif_ctx ctx, int64_t* first, int64_t* count);
 
+/* Host-only partition rule used by pif_init (no CUDA): space rank s of
+   space_size owns [first, first + count) of n_global particles. */
+pif_status pif_partition(int64_t n_global, int32_t space_size, int32_t s_idx, int64_t* first,
+                         int64_t* count);
+
 /* Device workspace: bytes needed (256-byte aligned base required), then hand
    over a caller-owned device buffer that outlives the context's use. */
 pif_status pif_workspace_size(pif_ctx ctx, size_t* bytes);
@@ -200,6 +205,27 @@ pif_status pif_debug_type2(pif_ctx ctx, int which, const double* c, const double
    if drift: x <- wrap(x + dt v).  Host pointers, in place. */
 pif_status pif_debug_push(pif_ctx ctx, int which, double* x, double* v, const double* E, int64_t n,
                           int kicks, int drift);
+
+/* Test-only: run the pipelined parareal protocol of time slice t of T (the
+   host logic of pif_parareal with time_size > 1: iteration-0 coarse sweep,
+   F / receive / G / correction / send per iteration, retirement when the
+   slice's e_x, e_v <= tol and its predecessor retired, frozen inputs once the
+   predecessor retired) over caller-supplied operations on buffer ids
+   0 = U_t, 1 = F(U_t), 2 = G_old, 3 = G_new, 4 = U_{t+1}.  Callbacks return 0
+   on success.  Outputs: iterations run, retired_at (1-based, -1 never),
+   err_x/err_v[max_iter] (NaN where not run), final_buf = id holding U_{t+1}. */
+typedef struct {
+  void* user;
+  int (*store_initial)(void* user, int dst);
+  int (*propagate)(void* user, int which, int src, int dst);
+  int (*correct)(void* user, int f, int gn, int go, int u, double* ex, double* ev);
+  int (*send)(void* user, int buf, double flag);
+  int (*recv)(void* user, int buf, double* flag);
+} pif_protocol_ops;
+pif_status pif_debug_parareal_protocol(int32_t t, int32_t T, int32_t max_iter, double tol,
+                                       const pif_protocol_ops* ops, int32_t* iterations,
+                                       int32_t* retired_at, double* err_x, double* err_v,
+                                       int32_t* final_buf);
 
 #ifdef __cplusplus
 }

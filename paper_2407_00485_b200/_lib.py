@@ -54,6 +54,7 @@ _sig = {
     "pif_init": [C.POINTER(PifPhysics), C.POINTER(PifPropagator), C.POINTER(PifPropagator), _i64,
                  C.POINTER(PifDist), C.POINTER(_ctx)],
     "pif_local_count": [_ctx, C.POINTER(_i64), C.POINTER(_i64)],
+    "pif_partition": [_i64, C.c_int32, C.c_int32, C.POINTER(_i64), C.POINTER(_i64)],
     "pif_workspace_size": [_ctx, C.POINTER(C.c_size_t)],
     "pif_set_workspace": [_ctx, C.c_void_p, C.c_size_t],
     "pif_set_state": [_ctx, _dp, _dp, _i64, C.c_int],
@@ -71,6 +72,10 @@ _sig = {
     "pif_debug_type2": [_ctx, C.c_int, _dp, _dp, _i64, _dp],
     "pif_debug_push": [_ctx, C.c_int, _dp, _dp, _dp, _i64, C.c_int, C.c_int],
     "pif_profile": [_ctx, C.c_int],
+    "pif_debug_parareal_protocol": [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p,
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_int32)],
     "pif_profile_read": [_ctx, C.POINTER(C.c_double), C.c_int32, C.POINTER(_i64), C.c_int],
 }
 for _name, _args in _sig.items():
@@ -151,6 +156,12 @@ def pif_init(phys, fine, coarse, n_particles_global, device=0, rank=0, world=1, 
 def pif_local_count(ctx):
     a, b = _i64(), _i64()
     _check("pif_local_count", lib.pif_local_count(ctx, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def pif_partition(n_global, space_size, s_idx):
+    a, b = _i64(), _i64()
+    _check("pif_partition", lib.pif_partition(n_global, space_size, s_idx, C.byref(a), C.byref(b)))
     return a.value, b.value
 
 

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -562,9 +563,7 @@ pif_status pif_init(const pif_physics* phys, const pif_propagator* fine,
   c->s_idx = dist->rank % dist->space_size;
   c->t_idx = dist->rank / dist->space_size;
   c->st = (cudaStream_t)dist->stream;
-  const int64_t base = n_particles_global / c->space_size, rem = n_particles_global % c->space_size;
-  c->nloc = base + (c->s_idx < rem ? 1 : 0);
-  c->first = c->s_idx * base + std::min<int64_t>(c->s_idx, rem);
+  pif_partition(n_particles_global, c->space_size, c->s_idx, &c->first, &c->nloc);
   auto bail = [&](pif_status s) {
     std::string msg = g_err;
     pif_finalize(c);
@@ -617,6 +616,16 @@ pif_status pif_init(const pif_physics* phys, const pif_propagator* fine,
     }
   }
   *out = c;
+  return PIF_OK;
+}
+
+pif_status pif_partition(int64_t n_global, int32_t space_size, int32_t s_idx, int64_t* first,
+                         int64_t* count) {
+  if (!first || !count || n_global < 0 || space_size < 1 || s_idx < 0 || s_idx >= space_size)
+    return fail(PIF_ERR_ARG, "bad partition arguments");
+  const int64_t base = n_global / space_size, rem = n_global % space_size;
+  *count = base + (s_idx < rem ? 1 : 0);
+  *first = s_idx * base + std::min<int64_t>(s_idx, rem);
   return PIF_OK;
 }
 
@@ -855,76 +864,78 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
     rep->converged = conv;
   } else {
     // ---------------- pipelined: slice t_idx on this time rank -------------
+    // The protocol (protocol.cu) is host logic; the operations below bind its
+    // buffer ids to device states and NCCL.
     const int t = c->t_idx, T = c->time_size;
-    double *U, *Fk, *Gold, *Gnew, *Unext;
-    if ((st = alloc(&U)) || (st = alloc(&Fk)) || (st = alloc(&Gold)) || (st = alloc(&Gnew)) ||
-        (st = alloc(&Unext))) {
-      free_all();
-      return st;
-    }
-    // send on the comm stream (ordered after the producer on st); any later
-    // write into a buffer waits for ev_sent (see guard()).
-    auto nsend = [&](const double* buf) -> pif_status {
+    double* buf[5];
+    for (auto& p : buf)
+      if ((st = alloc(&p)) != PIF_OK) { free_all(); return st; }
+    struct GpuOps {
+      pif_ctx c;
+      double** buf;
+      int t;
+      int64_t n, SZ;
+      double *t_fine, *t_coarse, *t_comm, *t_coarse0;
+      bool first_coarse;
+      std::function<pif_status(int, const double*, double*)> propagate;
+      std::function<pif_status(const double*, const double*, const double*, double*, double&, double&)> correct;
+      std::function<pif_status(double&, std::function<pif_status()>)> timed;
+    };
+    GpuOps G{c, buf, t, n, SZ, &t_fine, &t_coarse, &t_comm, &t_coarse0, true, propagate, correct,
+             [&](double& acc, std::function<pif_status()> fn) { return timed(acc, fn); }};
+    CU(cudaEventRecord(c->ev_sent, c->st));
+    ProtocolOps ops;
+    ops.user = &G;
+    ops.store_initial = [](void* u, int dst) -> pif_status {
+      auto* g = static_cast<GpuOps*>(u);
+      return store_state(g->c, g->buf[dst]);
+    };
+    ops.propagate = [](void* u, int which, int src, int dst) -> pif_status {
+      auto* g = static_cast<GpuOps*>(u);
+      double& acc = which == 0 ? *g->t_fine : (g->first_coarse ? *g->t_coarse0 : *g->t_coarse);
+      if (which == 1) g->first_coarse = false;
+      return g->timed(acc, [&] { return g->propagate(which, g->buf[src], g->buf[dst]); });
+    };
+    ops.correct = [](void* u, int f, int gn, int go, int un, double* ex, double* ev) -> pif_status {
+      auto* g = static_cast<GpuOps*>(u);
+      return g->correct(g->buf[f], g->buf[gn], g->buf[go], g->buf[un], *ex, *ev);
+    };
+    // send on the comm stream, ordered after the producer on st; guard() makes
+    // later writes into a sent buffer wait for ev_sent.
+    ops.send = [](void* u, int b, double flag) -> pif_status {
+      auto* g = static_cast<GpuOps*>(u);
+      pif_ctx c = g->c;
+      CU(cudaMemcpyAsync(g->buf[b] + 6 * g->n, &flag, sizeof(double), cudaMemcpyHostToDevice, c->st));
       CU(cudaEventRecord(c->ev_ready, c->st));
       CU(cudaStreamWaitEvent(c->st_comm, c->ev_ready, 0));
-      NC(ncclSend(buf, SZ, ncclDouble, t + 1, c->comm_tp[t % 2], c->st_comm));
+      NC(ncclSend(g->buf[b], g->SZ, ncclDouble, g->t + 1, c->comm_tp[g->t % 2], c->st_comm));
       CU(cudaEventRecord(c->ev_sent, c->st_comm));
       return PIF_OK;
     };
-    auto nrecv = [&](double* buf) -> pif_status {
-      NC(ncclRecv(buf, SZ, ncclDouble, t - 1, c->comm_tp[(t + 1) % 2], c->st));
-      return PIF_OK;
-    };
-    auto guard = [&]() -> pif_status {
-      CU(cudaStreamWaitEvent(c->st, c->ev_sent, 0));
-      return PIF_OK;
-    };
-    CU(cudaEventRecord(c->ev_sent, c->st));
-    bool pred_retired = (t == 0), retired = false, changed = true;
-    std::vector<double> myx(max_iter, NAN), myv(max_iter, NAN);
-    int my_ret = -1;
-    // iteration 0
-    if (t == 0) st = store_state(c, U);
-    else st = timed(t_comm, [&] { return nrecv(U); });
-    if (st == PIF_OK) st = timed(t_coarse0, [&] { return propagate(1, U, Gold); });
-    changed = false;
-    if (st == PIF_OK && t + 1 < T) st = timed(t_comm, [&] { return nsend(Gold); });
-    for (int k = 0; k < max_iter && st == PIF_OK && !retired; ++k) {
-      iterations = k + 1;
-      st = timed(t_fine, [&] { return propagate(0, U, Fk); });
-      if (st != PIF_OK) break;
-      if (!pred_retired) {
-        st = timed(t_comm, [&] { return nrecv(U); });
-        if (st != PIF_OK) break;
-        double flag = 0;
-        CU(cudaMemcpyAsync(&c->host_red[8], U + 6 * n, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    ops.recv = [](void* u, int b, double* flag) -> pif_status {
+      auto* g = static_cast<GpuOps*>(u);
+      pif_ctx c = g->c;
+      return g->timed(*g->t_comm, [&]() -> pif_status {
+        NC(ncclRecv(g->buf[b], g->SZ, ncclDouble, g->t - 1, c->comm_tp[(g->t + 1) % 2], c->st));
+        CU(cudaMemcpyAsync(&c->host_red[8], g->buf[b] + 6 * g->n, sizeof(double),
+                           cudaMemcpyDeviceToHost, c->st));
         CU(cudaStreamSynchronize(c->st));
-        flag = c->host_red[8];
-        if (flag != 0.0) pred_retired = true;
-        changed = true;
-      }
-      double* Gn = Gold;
-      if ((st = guard()) != PIF_OK) break;
-      if (changed) {
-        st = timed(t_coarse, [&] { return propagate(1, U, Gnew); });
-        if (st != PIF_OK) break;
-        Gn = Gnew;
-      }
-      double ex = 0, ev = 0;
-      st = correct(Fk, Gn, Gold, Unext, ex, ev);
-      if (st != PIF_OK) break;
-      changed = false;
-      if (Gn == Gnew) std::swap(Gold, Gnew);
-      myx[k] = ex;
-      myv[k] = ev;
-      if (ex <= stop_tol && ev <= stop_tol && pred_retired) {
-        retired = true;
-        my_ret = k + 1;
-      }
-      double fl = retired ? 1.0 : 0.0;
-      CU(cudaMemcpyAsync(Unext + 6 * n, &fl, sizeof(double), cudaMemcpyHostToDevice, c->st));
-      if (t + 1 < T) st = timed(t_comm, [&] { return nsend(Unext); });
-    }
+        *flag = c->host_red[8];
+        return PIF_OK;
+      });
+    };
+    ops.guard = [](void* u) -> pif_status {
+      auto* g = static_cast<GpuOps*>(u);
+      CU(cudaStreamWaitEvent(g->c->st, g->c->ev_sent, 0));
+      return PIF_OK;
+    };
+    ProtocolResult pr;
+    st = run_pipeline(t, T, max_iter, stop_tol, ops, pr);
+    iterations = pr.iterations;
+    double* Unext = buf[pr.final_buf];
+    std::vector<double>& myx = pr.ex;
+    std::vector<double>& myv = pr.ev;
+    int my_ret = pr.retired_at;
     if (c->st_comm) cudaStreamSynchronize(c->st_comm);
     if (st == PIF_OK) st = load_state(c, Unext);
     // gather the report over the time group (small)

@@ -178,4 +178,23 @@ cudaError_t launch_correct_norms(const double* F, const double* Gn, const double
 cudaError_t launch_check_finite(const double* a, int64_t count, int* flag, cudaStream_t st);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
+
+// ---------------------------------------- parareal pipeline protocol (host) --
+// Buffer ids of one time slice: input U_t, F(U_t), G(U_t^k), G(U_t^{k+1}), U_{t+1}.
+enum { PB_U = 0, PB_F = 1, PB_GOLD = 2, PB_GNEW = 3, PB_UNEXT = 4 };
+struct ProtocolOps {
+  void* user;
+  pif_status (*store_initial)(void* user, int dst);               // current state -> dst (t == 0)
+  pif_status (*propagate)(void* user, int which, int src, int dst); // 0 = F, 1 = G
+  pif_status (*correct)(void* user, int F, int Gn, int Go, int U, double* ex, double* ev);
+  pif_status (*send)(void* user, int buf, double flag);            // to t + 1
+  pif_status (*recv)(void* user, int buf, double* flag);           // from t - 1
+  pif_status (*guard)(void* user);  // later writes must wait for in-flight sends
+};
+struct ProtocolResult {
+  int iterations = 0, retired_at = -1, final_buf = 0;
+  std::vector<double> ex, ev;
+};
+pif_status run_pipeline(int t, int T, int max_iter, double tol, const ProtocolOps& ops,
+                        ProtocolResult& res);
 }  // namespace pif
