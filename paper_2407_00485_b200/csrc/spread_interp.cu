@@ -51,7 +51,7 @@ template <int RX, int RY, int RZ>
 struct Psi {
   double px[kChunk][RowStride<RX>::v];
   double py[kChunk][RowStride<RY>::v];
-  double pz[kChunk][RowStride<RZ>::v];
+  double pz[kChunk][RowStride<(RZ + 7) / 8 * 8>::v];  // z rows zero-padded to a multiple of 8
   double xs[kChunk][3];
   int rel[kChunk][3];
   double str[kChunk];
@@ -108,7 +108,7 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ>& sm, int cnt, int pad,
   const int w = g.w;
   for (int it = threadIdx.x; it < 3 * pad; it += blockDim.x) {
     const int d = it / pad, p = it - d * pad;
-    const int R = d == 0 ? RX : (d == 1 ? RY : RZ);
+    const int R = d == 0 ? RX : (d == 1 ? RY : (RZ + 7) / 8 * 8);
     double* row = d == 0 ? sm.px[p] : (d == 1 ? sm.py[p] : sm.pz[p]);
     if (p >= cnt) {
       for (int u = 0; u < R; ++u) row[u] = 0.0;
@@ -142,10 +142,11 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ>& sm, int cnt, int pad,
 // ------------------------------------------------------------------ spread --
 template <int RX, int RY, int RZ>
 struct SpreadCfg {
-  static constexpr int CT = 4;                    // column tiles (of 8) per warp
-  static constexpr int NW = RX * RY / (8 * CT);   // warps
-  static constexpr int ZT = RZ / 8;               // z tiles (of 8)
-  static_assert(RX * RY % (8 * CT) == 0 && RZ % 8 == 0, "tile shape");
+  static constexpr int NCT = RX * RY / 8;         // column tiles (of 8)
+  static constexpr int CT = NCT % 4 == 0 ? 4 : 3; // column tiles per warp
+  static constexpr int NW = NCT / CT;             // warps
+  static constexpr int ZT = (RZ + 7) / 8;         // z tiles of 8 (psi_z rows zero-padded)
+  static_assert(RX * RY % 8 == 0 && NCT % CT == 0, "tile shape");
 };
 
 template <int RX, int RY, int RZ, bool HAS_S>
@@ -210,8 +211,9 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
     for (int zt = 0; zt < C::ZT; ++zt)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        double val = acc[ct][zt][i];
-        if (val != 0.0) atomicAdd(colp + wrapi(T0[2] + zt * 8 + 2 * tq + i, n), val * s_uniform);
+        const double val = acc[ct][zt][i];
+        const int z = zt * 8 + 2 * tq + i;
+        if (z < RZ && val != 0.0) atomicAdd(colp + wrapi(T0[2] + z, n), val * s_uniform);
       }
   }
 }
@@ -219,10 +221,11 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
 // ------------------------------------------------------------ interp+push --
 template <int RX, int RY, int RZ>
 struct InterpCfg {
-  static constexpr int CT = 4;                    // column tiles (of 8) per warp
-  static constexpr int NW = RX * RY / (8 * CT);   // warps
+  static constexpr int NCT = RX * RY / 8;         // column tiles (of 8)
+  static constexpr int CT = NCT % 4 == 0 ? 4 : 3; // column tiles per warp
+  static constexpr int NW = NCT / CT;             // warps
   static constexpr int KS = RZ / 4;               // k steps (z) per MMA chain
-  static_assert(RX * RY % (8 * CT) == 0 && RZ % 4 == 0, "tile shape");
+  static_assert(RX * RY % 8 == 0 && NCT % CT == 0 && RZ % 4 == 0, "tile shape");
 };
 
 template <int RX, int RY, int RZ>
@@ -393,7 +396,7 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
     return cudaGetLastError();                                                                \
   }
   PIF_SPREAD(8, 8, 8)
-  PIF_SPREAD(16, 14, 16)
+  PIF_SPREAD(12, 12, 12)
   PIF_SPREAD(16, 16, 16)
 #undef PIF_SPREAD
   return cudaErrorInvalidValue;
@@ -425,6 +428,7 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
   PIF_INTERP(8, 8, 8)
+  PIF_INTERP(12, 12, 12)
   PIF_INTERP(16, 14, 16)
   PIF_INTERP(16, 16, 16)
 #undef PIF_INTERP
