@@ -615,6 +615,26 @@ pif_status pif_init(const pif_physics* phys, const pif_propagator* fine,
       fail(PIF_ERR_CUDA, std::string("comm stream: ") + cudaGetErrorString(e));
       return bail(PIF_ERR_CUDA);
     }
+    // Establish the t -> t+1 peer connections now (NCCL connects lazily on the
+    // first send/recv), so that pif_parareal's timing excludes setup.
+    double* tmp = nullptr;
+    e = cudaMalloc(&tmp, 2 * sizeof(double));
+    if (e != cudaSuccess) {
+      fail(PIF_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+      return bail(PIF_ERR_CUDA);
+    }
+    const int t = c->t_idx, T = c->time_size;
+    ncclResult_t r = ncclGroupStart();
+    if (r == ncclSuccess && t + 1 < T) r = ncclSend(tmp, 1, ncclDouble, t + 1, c->comm_tp[t % 2], c->st);
+    if (r == ncclSuccess && t > 0) r = ncclRecv(tmp + 1, 1, ncclDouble, t - 1, c->comm_tp[(t + 1) % 2], c->st);
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r == ncclSuccess) r = r2;
+    e = cudaStreamSynchronize(c->st);
+    cudaFree(tmp);
+    if (r != ncclSuccess || e != cudaSuccess) {
+      fail(PIF_ERR_NCCL, "parareal peer warm-up failed");
+      return bail(PIF_ERR_NCCL);
+    }
   }
   *out = c;
   return PIF_OK;
