@@ -28,21 +28,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    if out is None and not force and up_to_date():
         return LIB
+    target = out or LIB
     cmd = [NVCC, "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC,-O3", "-shared",
            "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
            "-Xptxas", "-v" if verbose else "-O3",
-           *sources(), "-o", LIB + ".tmp", "-lcufft", "-lnccl"]
+           *[f"-D{d}" for d in defines], *sources(), "-o", target + ".tmp", "-lcufft", "-lnccl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libpif.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

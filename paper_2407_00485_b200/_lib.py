@@ -11,7 +11,8 @@ import os
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpif.so")
+_LIB_PATH = os.environ.get("PIF_LIBRARY") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libpif.so")  # override: kernel A/B experiments
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
         f"{_LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "

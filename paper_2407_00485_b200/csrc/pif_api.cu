@@ -280,7 +280,7 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     int RI[3], m[3] = {1, 1, 1};
     if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
     else if (w <= 9) { RI[0] = RI[1] = RI[2] = 12; }
-    else if (w == 13) { RI[0] = 16; RI[1] = 14; RI[2] = 16; m[1] = 2; }
+    else if (w == 13) { RI[0] = 14; RI[1] = 14; RI[2] = 16; m[0] = m[1] = 2; }
     else { RI[0] = RI[1] = RI[2] = 16; }
     Brick& g = p.g;
     g.n = n;

@@ -29,15 +29,35 @@
 
 namespace pif {
 
-constexpr int kChunk = 64;  // particles staged per shared-memory round (multiple of 8)
+#ifndef PIF_CHUNK
+#define PIF_CHUNK 128
+#endif
+#ifndef PIF_ICHUNK
+#define PIF_ICHUNK 64
+#endif
+constexpr int kChunk = PIF_CHUNK;    // spread: particles staged per shared-memory round
+constexpr int kIChunk = PIF_ICHUNK;  // interp: smaller, so two CTAs fit per SM
 
+#ifdef PIF_DMMA_NONVOLATILE
+#define PIF_DMMA_ASM asm
+#else
+#define PIF_DMMA_ASM asm volatile
+#endif
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  PIF_DMMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ int wrapi(int i, int n) { return ((i % n) + n) % n; }
+
+// 8-byte asynchronous global -> shared copy (LDGSTS; no register staging).
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // psi row strides (doubles): S == 4 or 12 (mod 16) so that the 4 particle rows
 // read by one half-warp fragment load (4 consecutive doubles each) fall in
@@ -47,14 +67,14 @@ struct RowStride {
   static constexpr int v = R <= 8 ? 12 : (R <= 16 ? 20 : ((R + 11) / 16) * 16 + 4);
 };
 
-template <int RX, int RY, int RZ>
+template <int RX, int RY, int RZ, int CH = kChunk>
 struct Psi {
-  double px[kChunk][RowStride<RX>::v];
-  double py[kChunk][RowStride<RY>::v];
-  double pz[kChunk][RowStride<(RZ + 7) / 8 * 8>::v];  // z rows zero-padded to a multiple of 8
-  double xs[kChunk][3];
-  int rel[kChunk][3];
-  double str[kChunk];
+  double px[CH][RowStride<RX>::v];
+  double py[CH][RowStride<RY>::v];
+  double pz[CH][RowStride<(RZ + 7) / 8 * 8>::v];  // z rows zero-padded to a multiple of 8
+  double xs[CH][3];
+  int rel[CH][3];
+  double str[CH];
 };
 
 // Decode a spread brick (sub == false) or interpolation sub-brick (sub == true)
@@ -83,8 +103,8 @@ __device__ __forceinline__ void tile_of(const Brick& g, int cta, bool sub, int T
 }
 
 // Thread tid < cnt: record particle tid's grid coordinate and window offset.
-template <int RX, int RY, int RZ>
-__device__ __forceinline__ void stage_position(Psi<RX, RY, RZ>& sm, int tid, const double xr[3],
+template <int RX, int RY, int RZ, int CH>
+__device__ __forceinline__ void stage_position(Psi<RX, RY, RZ, CH>& sm, int tid, const double xr[3],
                                                const Brick& g, const int T0[3]) {
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
@@ -99,31 +119,44 @@ __device__ __forceinline__ void stage_position(Psi<RX, RY, RZ>& sm, int tid, con
 // cnt .. pad-1 get zero rows.  One item per (dimension, particle): the w window
 // weights by per-node Horner polynomials (edge nodes exactly), zeros elsewhere
 // in the tile row.  Starts and ends with __syncthreads().
-template <int RX, int RY, int RZ>
-__device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ>& sm, int cnt, int pad, const Brick& g,
+template <bool SPLIT, int RX, int RY, int RZ, int CH>
+__device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int pad, const Brick& g,
                                           const int T0[3], const Horner& hc) {
   __syncthreads();
   const double two_over_w = 2.0 / g.w;
   const double flo = g.odd ? -0.5 : 0.0;
   const int w = g.w;
-  for (int it = threadIdx.x; it < 3 * pad; it += blockDim.x) {
-    const int d = it / pad, p = it - d * pad;
+  const int ngroups = (w - 2 + 3) / 4;  // groups of 4 interior nodes (>= 1 for w >= 3)
+  // SPLIT: one item per (group, dim, particle) -- more parallelism for big CTAs;
+  // else one item per (dim, particle) looping over its groups.
+  const int ng = SPLIT ? ngroups : 1;
+  // group-major item order: a warp's lanes share (grp, d), so the Horner
+  // coefficient reads are warp-uniform (constant-cache broadcast)
+  const int per_g = 3 * pad;
+  for (int it = threadIdx.x; it < ng * per_g; it += blockDim.x) {
+    const int grp = it / per_g;
+    const int rem = it - grp * per_g;
+    const int d = rem / pad, p = rem - d * pad;
     const int R = d == 0 ? RX : (d == 1 ? RY : (RZ + 7) / 8 * 8);
     double* row = d == 0 ? sm.px[p] : (d == 1 ? sm.py[p] : sm.pz[p]);
     if (p >= cnt) {
-      for (int u = 0; u < R; ++u) row[u] = 0.0;
+      if (grp == 0)
+        for (int u = 0; u < R; ++u) row[u] = 0.0;
       continue;
     }
     const int rel = sm.rel[p][d];
     const int T0d = d == 0 ? T0[0] : (d == 1 ? T0[1] : T0[2]);
     const double f = sm.xs[p][d] - (double)(rel + g.hw + T0d);  // x~ - anchor
+    if (grp == 0) {
+      for (int u = 0; u < rel; ++u) row[u] = 0.0;
+      for (int u = rel + w; u < R; ++u) row[u] = 0.0;
+      row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
+      row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+    }
+    // interior nodes k0 .. k0+3 of a group: four independent Horner chains
     const double sv = 2.0 * (f - flo) - 1.0;
-    for (int u = 0; u < rel; ++u) row[u] = 0.0;
-    for (int u = rel + w; u < R; ++u) row[u] = 0.0;
-    row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
-    row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
-    // interior nodes 1 .. w-2, four independent Horner chains at a time
-    for (int k0 = 1; k0 < w - 1; k0 += 4) {
+    for (int gg = SPLIT ? grp : 0; gg < (SPLIT ? grp + 1 : ngroups); ++gg) {
+      const int k0 = 1 + 4 * gg;
       double acc[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[q] = hc.a[min(k0 + q, 15)][kHornerDeg];
@@ -155,7 +188,8 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
              double s_uniform, const int* __restrict__ offsets, Brick g,
              const __grid_constant__ Horner hc, double* __restrict__ grid) {
   using C = SpreadCfg<RX, RY, RZ>;
-  __shared__ Psi<RX, RY, RZ> sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Psi<RX, RY, RZ>& sm = *reinterpret_cast<Psi<RX, RY, RZ>*>(smem_raw);
   int T0[3];
   int64_t start, end;
   tile_of(g, blockIdx.x, false, T0, offsets, start, end);
@@ -179,12 +213,12 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
   for (int64_t base = start; base < end; base += kChunk) {
     const int cnt = (int)min((int64_t)kChunk, end - base);
     const int pad = (cnt + 3) & ~3;
-    if (tid < cnt) {
-      double xr[3] = {x[base + tid], x[stride + base + tid], x[2 * stride + base + tid]};
-      stage_position(sm, tid, xr, g, T0);
-      if (HAS_S) sm.str[tid] = s[base + tid];
+    for (int q = tid; q < cnt; q += blockDim.x) {
+      double xr[3] = {x[base + q], x[stride + base + q], x[2 * stride + base + q]};
+      stage_position(sm, q, xr, g, T0);
+      if (HAS_S) sm.str[q] = s[base + q];
     }
-    stage_psi(sm, cnt, pad, g, T0, hc);
+    stage_psi<false>(sm, cnt, pad, g, T0, hc);
     for (int p0 = 0; p0 < pad; p0 += 4) {
       const int pl = p0 + tq;  // K index of this lane's A and B elements
       double b[C::ZT];
@@ -219,23 +253,37 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
 }
 
 // ------------------------------------------------------------ interp+push --
+// "K = columns" formulation: every warp owns whole m-tiles of 8 particles and
+// contracts over all tile columns,
+//   T_d[p][z] = sum_c W[p][c] g_d[c][z],   W[p][c] = psi_x[p][cx] psi_y[p][cy]
+// (M = particles, K = columns, N = z), with the g tile staged once per CTA in
+// shared memory in B-fragment order (one conflict-free LDS.64 per DMMA) and A
+// formed by one DMUL per fragment element.  Stage 2, E_d[p] = sum_z psi_z[p][z]
+// T_d[p][z], is 16 values per particle inside the warp; the warp pushes its own
+// particles, so the m-tile loop has no block barrier.  DMMA and DFMA share the
+// FP64 pipe on B200 (profiles/r1_dmma_mix.log), so the vector work is kept to
+// ~3 % of the MMA FMAs.
 template <int RX, int RY, int RZ>
 struct InterpCfg {
-  static constexpr int NCT = RX * RY / 8;         // column tiles (of 8)
-  static constexpr int CT = NCT % 4 == 0 ? 4 : 3; // column tiles per warp
-  static constexpr int NW = NCT / CT;             // warps
-  static constexpr int KS = RZ / 4;               // k steps (z) per MMA chain
-  static_assert(RX * RY % 8 == 0 && NCT % CT == 0 && RZ % 4 == 0, "tile shape");
+  static constexpr int NC = RX * RY;       // tile columns (K)
+  static constexpr int KS = NC / 4;        // k steps
+  static constexpr int NT = (RZ + 7) / 8;  // z n-tiles of 8 (psi_z rows zero-padded)
+#ifndef PIF_INW
+#define PIF_INW 8
+#endif
+  static constexpr int NW = PIF_INW;       // warps (m-tiles processed round-robin)
+  static_assert(NC % 4 == 0, "tile columns must be a multiple of 4");
 };
 
 template <int RX, int RY, int RZ>
 struct InterpSmem {
-  Psi<RX, RY, RZ> psi;
-  double red[kChunk][InterpCfg<RX, RY, RZ>::NW][3];
+  double gB[InterpCfg<RX, RY, RZ>::KS][InterpCfg<RX, RY, RZ>::NT][3][32];  // B fragments
+  Psi<RX, RY, RZ, kIChunk> psi;
+  double xv[2][6][kIChunk];  // x, v of the current / next chunk (cp.async double buffer)
 };
 
 template <int RX, int RY, int RZ>
-__global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
+__global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
     k_interp_push(const double* __restrict__ grid3, double* __restrict__ x,
                   double* __restrict__ v, int64_t stride, const int* __restrict__ id,
                   double* __restrict__ Eout, const int* __restrict__ offsets, Brick g,
@@ -243,7 +291,7 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
   using C = InterpCfg<RX, RY, RZ>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   InterpSmem<RX, RY, RZ>& S = *reinterpret_cast<InterpSmem<RX, RY, RZ>*>(smem_raw);
-  Psi<RX, RY, RZ>& sm = S.psi;
+  Psi<RX, RY, RZ, kIChunk>& sm = S.psi;
   int T0[3];
   int64_t start, end;
   tile_of(g, blockIdx.x, true, T0, offsets, start, end);
@@ -252,149 +300,139 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW)
   const int gr = lane >> 2, tq = lane & 3;
   const int n = g.n;
   const int64_t n3 = (int64_t)n * n * n;
-  // B fragments: B[k = tq][col = gr] = g_d[z = ks*4 + tq][c = (wid*CT+ct)*8 + gr]
-  double gb[C::CT][C::KS][3];
+
+  // x, v of chunk i+1 stream into S.xv[(i+1)&1] with cp.async during chunk i
+  auto prefetch = [&](int buf, int64_t b, int c) {
+    for (int r = tid; r < c; r += blockDim.x) {
+      const int64_t j = b + r;
 #pragma unroll
-  for (int ct = 0; ct < C::CT; ++ct) {
-    int c = (wid * C::CT + ct) * 8 + gr;
-    const int64_t cb = ((int64_t)wrapi(T0[0] + c % RX, n) * n + wrapi(T0[1] + c / RX, n)) * n;
+      for (int q = 0; q < 3; ++q) cp_async8(&S.xv[buf][q][r], x + q * stride + j);
+      if (v)
 #pragma unroll
-    for (int ks = 0; ks < C::KS; ++ks) {
-      int gz = wrapi(T0[2] + ks * 4 + tq, n);
-      gb[ct][ks][0] = grid3[cb + gz];
-      gb[ct][ks][1] = grid3[n3 + cb + gz];
-      gb[ct][ks][2] = grid3[2 * n3 + cb + gz];
+        for (int q = 0; q < 3; ++q) cp_async8(&S.xv[buf][3 + q][r], v + q * stride + j);
+    }
+    cp_async_commit();
+  };
+  prefetch(0, start, (int)min((int64_t)kIChunk, end - start));
+
+  // g tile -> B fragments: gB[ks][nt][d][l] = g_d[c = 4 ks + (l & 3)][z = 8 nt + (l >> 2)]
+  // (consecutive threads read consecutive z of one column: coalesced)
+  {
+    // one (component, column) pair per 16 lanes: each lane one z of the column
+    constexpr int ZP = C::NT * 8;           // padded z extent (8 or 16)
+    constexpr int PER = 32 / ZP;            // (d, c) pairs per warp step
+    const int zl = lane % ZP, sub = lane / ZP;
+    int gz = T0[2] + zl;
+    gz = gz < 0 ? gz + n : (gz >= n ? gz - n : gz);
+    for (int dc = wid * PER + sub; dc < 3 * C::NC; dc += C::NW * PER) {
+      const int d = dc / C::NC, c = dc - d * C::NC;
+      const int cy = c / RX, cx = c - cy * RX;
+      int gx = T0[0] + cx, gy = T0[1] + cy;
+      gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
+      gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
+      const double val = zl < RZ ? grid3[d * n3 + ((int64_t)gx * n + gy) * n + gz] : 0.0;
+      S.gB[c >> 2][zl >> 3][d][((zl & 7) << 2) | (c & 3)] = val;
     }
   }
-  // C-fragment columns of this lane: c = (wid*CT+ct)*8 + 2*tq + i
-  int ccx[C::CT][2], ccy[C::CT][2];
-#pragma unroll
-  for (int ct = 0; ct < C::CT; ++ct)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      int c = (wid * C::CT + ct) * 8 + 2 * tq + i;
-      ccx[ct][i] = c % RX;
-      ccy[ct][i] = c / RX;
-    }
 
-  // x, v of the next chunk are prefetched into registers during the MMA phase
-  double xn[3] = {0, 0, 0}, vn[3] = {0, 0, 0};
-  auto fetch = [&](int64_t b, int c) {
-    if (tid < c) {
-      const int64_t j = b + tid;
-      xn[0] = x[j];
-      xn[1] = x[stride + j];
-      xn[2] = x[2 * stride + j];
-      if (v) {
-        vn[0] = v[j];
-        vn[1] = v[stride + j];
-        vn[2] = v[2 * stride + j];
-      }
-    }
-  };
-  fetch(start, (int)min((int64_t)kChunk, end - start));
-  for (int64_t base = start; base < end; base += kChunk) {
-    const int cnt = (int)min((int64_t)kChunk, end - base);
+  int buf = 0;
+  for (int64_t base = start; base < end; base += kIChunk, buf ^= 1) {
+    const int cnt = (int)min((int64_t)kIChunk, end - base);
     const int pad = (cnt + 7) & ~7;
-    double xr[3] = {xn[0], xn[1], xn[2]}, vr[3] = {vn[0], vn[1], vn[2]};
-    if (tid < cnt) stage_position(sm, tid, xr, g, T0);
-    stage_psi(sm, cnt, pad, g, T0, hc);
-    if (base + kChunk < end) fetch(base + kChunk, (int)min((int64_t)kChunk, end - base - kChunk));
-    // Software-pipelined over m-tiles of 8 particles: the DMMAs of tile i+1 are
-    // issued before the vector-pipe stage 2 of tile i consumes its accumulators.
-    auto mma_tile = [&](int p0, double (&acc)[C::CT][3][2]) {
+    cp_async_wait_all();
+    __syncthreads();  // every thread's cp.async data for this chunk is visible
+    for (int q = tid; q < cnt; q += blockDim.x) {
+      const double xr[3] = {S.xv[buf][0][q], S.xv[buf][1][q], S.xv[buf][2][q]};
+      stage_position(sm, q, xr, g, T0);
+    }
+    stage_psi<true>(sm, cnt, pad, g, T0, hc);  // its barriers also publish gB
+    if (base + kIChunk < end) prefetch(buf ^ 1, base + kIChunk, (int)min((int64_t)kIChunk, end - base - kIChunk));
+    for (int p0 = 8 * wid; p0 < pad; p0 += 8 * C::NW) {
+      const int pa = p0 + gr;  // A row (particle) of this lane
+      double acc[C::NT][3][2];
 #pragma unroll
-      for (int ct = 0; ct < C::CT; ++ct)
+      for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) acc[ct][d][0] = acc[ct][d][1] = 0.0;
-#pragma unroll
+        for (int d = 0; d < 3; ++d) acc[nt][d][0] = acc[nt][d][1] = 0.0;
+#pragma unroll 4
       for (int ks = 0; ks < C::KS; ++ks) {
-        const double a = sm.pz[p0 + gr][ks * 4 + tq];  // A[g][t] = psi_z[p0+g][z]
+        const int c = 4 * ks + tq;
+        const double a = sm.px[pa][c % RX] * sm.py[pa][c / RX];  // A[g][t] = W[p0+g][4ks+t]
 #pragma unroll
-        for (int ct = 0; ct < C::CT; ++ct)
+        for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) dmma(acc[ct][d], a, gb[ct][ks][d]);
+          for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, S.gB[ks][nt][d][lane]);
       }
-    };
-    auto stage2 = [&](int p0, const double (&acc)[C::CT][3][2]) {
-      const int p = p0 + gr;
+      // stage 2: C[g][2t+i] = T_d[p0+g][z = 8nt + 2t + i]
       double e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
-      for (int ct = 0; ct < C::CT; ++ct)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const double W = sm.px[p][ccx[ct][i]] * sm.py[p][ccy[ct][i]];
-          e0 = fma(W, acc[ct][0][i], e0);
-          e1 = fma(W, acc[ct][1][i], e1);
-          e2 = fma(W, acc[ct][2][i], e2);
-        }
+      for (int nt = 0; nt < C::NT; ++nt) {
+        const double2 wz = *reinterpret_cast<const double2*>(&sm.pz[pa][8 * nt + 2 * tq]);
+        e0 = fma(wz.x, acc[nt][0][0], fma(wz.y, acc[nt][0][1], e0));
+        e1 = fma(wz.x, acc[nt][1][0], fma(wz.y, acc[nt][1][1], e1));
+        e2 = fma(wz.x, acc[nt][2][0], fma(wz.y, acc[nt][2][1], e2));
+      }
 #pragma unroll
       for (int o = 1; o <= 2; o <<= 1) {
         e0 += __shfl_xor_sync(0xffffffffu, e0, o);
         e1 += __shfl_xor_sync(0xffffffffu, e1, o);
         e2 += __shfl_xor_sync(0xffffffffu, e2, o);
       }
-      if (tq == 0) {
-        S.red[p][wid][0] = e0;
-        S.red[p][wid][1] = e1;
-        S.red[p][wid][2] = e2;
-      }
-    };
-    {
-      double accA[C::CT][3][2], accB[C::CT][3][2];
-      mma_tile(0, accA);
-      int p0 = 0;
-      for (; p0 + 16 <= pad; p0 += 16) {
-        mma_tile(p0 + 8, accB);
-        stage2(p0, accA);
-        if (p0 + 16 < pad) mma_tile(p0 + 16, accA);
-        stage2(p0 + 8, accB);
-      }
-      if (p0 < pad) stage2(p0, accA);  // pad % 16 == 8: last tile pending in accA
-    }
-    __syncthreads();
-    if (tid < cnt) {
-      double E0 = 0.0, E1 = 0.0, E2 = 0.0;
-#pragma unroll
-      for (int w = 0; w < C::NW; ++w) {
-        E0 += S.red[tid][w][0];
-        E1 += S.red[tid][w][1];
-        E2 += S.red[tid][w][2];
-      }
-      const int64_t j = base + tid;
-      if (Eout) {
-        const int64_t k = id[j];
-        Eout[k] = E0;
-        Eout[stride + k] = E1;
-        Eout[2 * stride + k] = E2;
-      }
-      if (P.kicks > 0 || P.drift) {
-        push_particle(xr[0], xr[1], xr[2], vr[0], vr[1], vr[2], E0, E1, E2, P);
-        x[j] = xr[0];
-        x[stride + j] = xr[1];
-        x[2 * stride + j] = xr[2];
-        v[j] = vr[0];
-        v[stride + j] = vr[1];
-        v[2 * stride + j] = vr[2];
+      if (tq == 0 && pa < cnt) {
+        const int64_t j = base + pa;
+        if (Eout) {
+          const int64_t k = id[j];
+          Eout[k] = e0;
+          Eout[stride + k] = e1;
+          Eout[2 * stride + k] = e2;
+        }
+        if (P.kicks > 0 || P.drift) {
+          double x0 = S.xv[buf][0][pa], x1 = S.xv[buf][1][pa], x2 = S.xv[buf][2][pa];
+          double v0 = S.xv[buf][3][pa], v1 = S.xv[buf][4][pa], v2 = S.xv[buf][5][pa];
+          push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
+          x[j] = x0;
+          x[stride + j] = x1;
+          x[2 * stride + j] = x2;
+          v[j] = v0;
+          v[stride + j] = v1;
+          v[2 * stride + j] = v2;
+        }
       }
     }
-    __syncthreads();
+    __syncthreads();  // psi rows / S.xv[buf] are reused by the next chunks
   }
+}
+
+template <int A, int B, int Cz>
+static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, const double* s,
+                                 double s_uniform, const int* offsets, const Brick& g,
+                                 const Horner& hc, double* grid, cudaStream_t st) {
+  const int T = 32 * SpreadCfg<A, B, Cz>::NW;
+  const size_t smem = sizeof(Psi<A, B, Cz, kChunk>);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_spread<A, B, Cz, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_spread<A, B, Cz, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (s)
+    k_spread<A, B, Cz, true><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+  else
+    k_spread<A, B, Cz, false><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
                           const int* offsets, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st) {
   const unsigned nbr = (unsigned)((int64_t)g.NB[0] * g.NB[1] * g.NB[2]);
-#define PIF_SPREAD(A, B, Cz)                                                                  \
-  if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz) {                                        \
-    const int T = 32 * SpreadCfg<A, B, Cz>::NW;                                               \
-    if (s)                                                                                    \
-      k_spread<A, B, Cz, true><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid); \
-    else                                                                                      \
-      k_spread<A, B, Cz, false><<<nbr, T, 0, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid); \
-    return cudaGetLastError();                                                                \
-  }
+#define PIF_SPREAD(A, B, Cz)                                        \
+  if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz)                \
+    return spread_launch<A, B, Cz>(nbr, x, stride, s, s_uniform, offsets, g, hc, grid, st);
   PIF_SPREAD(8, 8, 8)
   PIF_SPREAD(12, 12, 12)
   PIF_SPREAD(16, 16, 16)
@@ -429,7 +467,7 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
   PIF_INTERP(8, 8, 8)
   PIF_INTERP(12, 12, 12)
-  PIF_INTERP(16, 14, 16)
+  PIF_INTERP(14, 14, 16)
   PIF_INTERP(16, 16, 16)
 #undef PIF_INTERP
   return cudaErrorInvalidValue;
