@@ -64,6 +64,7 @@ typedef enum {
 } pif_status;
 
 typedef enum { PIF_PROP_PIF_NUFFT = 0, PIF_PROP_PIC_CIC = 1 } pif_prop_kind;
+#define PIF_FLAG_FP32_ALLREDUCE 1
 
 /* One propagator (fine F or coarse G of Sec. "Parareal for PIF"). */
 typedef struct {
@@ -73,6 +74,10 @@ typedef struct {
   int32_t spline_order; /* B-spline order m >= 1 of the shape function: S_k = prod_d
                            sinc^(m+1)(k_d h / 2), h = L / n.
                            PIC supports m = 1 (CIC) only. */
+  int32_t flags;        /* bit 0 PIF_FLAG_FP32_ALLREDUCE: all-reduce the density (PIF rho_hat
+                           box / PIC grid) over the space group in fp32 instead of fp64 --
+                           halves the communication, the "single precision for the density
+                           field" of P:553-554 (meant for coarse propagators).  0 = default. */
   double tol;           /* PIF: NUFFT tolerance eps in [1e-15, 1e-1); ignored for PIC */
   double dt;            /* timestep > 0 */
 } pif_propagator;
@@ -144,6 +149,13 @@ pif_status pif_step(pif_ctx ctx, int which, int64_t n_steps);
 pif_status pif_field_energy(pif_ctx ctx, double W[3], double* kinetic, double momentum[3],
                             double* charge_err);
 
+/* Density spectrum at the current integer time level (fine PIF propagator):
+   rho_tilde_k = (q / L^3) sum_j exp(-i k.x_j) (eq. scatter_pif without S_k, before
+   background removal, summed over the space group) on the Hermitian half box
+   mx, my in [-N/2, N/2], mz in [0, N/2]: out[2*(((mx+N/2)*(N+1) + my+N/2)*(N/2+1) + mz)]
+   = (re, im); host pointer of 2 (N+1)^2 (N/2+1) doubles.  Synchronises. */
+pif_status pif_get_rho(pif_ctx ctx, double* out);
+
 /* Parareal report; arrays are caller-allocated. */
 typedef struct {
   int32_t iterations;  /* correction iterations run (>= 1 when max_iter >= 1) */
@@ -163,8 +175,13 @@ typedef struct {
    and slice n-1 retired; retired slices are frozen.
    time_size == 1: all slices run serially on this rank (reference schedule);
    time_size > 1: n_slices must equal time_size (one slice per time rank,
-   states passed by NCCL send/recv).  n_blocks must be 1 (windowed parareal is
-   not implemented -> PIF_ERR_CONFIG).  Synchronises. */
+   states passed by NCCL send/recv).  n_blocks >= 1: multi-block parareal
+   (reading R22) -- [t0, t1] is cut into n_blocks equal windows
+   solved one after the other, each by parareal with n_slices slices, the final
+   state of a window seeding the next (broadcast from the last time rank).  The
+   report then holds the total iterations over windows, converged = all windows
+   converged, summed timings, and retired_at / err_x / err_v of the last window.
+   Synchronises. */
 pif_status pif_parareal(pif_ctx ctx, double t0, double t1, int32_t n_slices, int32_t max_iter,
                         double stop_tol, int32_t n_blocks, pif_parareal_report* report);
 

@@ -436,6 +436,22 @@ def parareal_serial(u0, F, G, n_slices: int, max_iter: int, tol: float, L=None):
     return PararealResult(U=U, iterations=it, retired_at=retired_at, err_x=errx, err_v=errv)
 
 
+def parareal_blocks(u0, make_F, make_G, n_slices: int, n_blocks: int, max_iter: int, tol: float,
+                    L=None):
+    """Multi-block (windowed) parareal (reading R22): the time
+    domain is cut into n_blocks equal windows solved one after the other, each by
+    parareal_serial with n_slices slices; a window's U_{n_slices} seeds the next.
+    make_F / make_G: window index -> propagator (the slice length is the same
+    for every window).  Returns the list of per-window PararealResults."""
+    out = []
+    u = u0
+    for b in range(n_blocks):
+        res = parareal_serial(u, make_F(b), make_G(b), n_slices, max_iter, tol, L)
+        out.append(res)
+        u = res.U[n_slices]
+    return out
+
+
 def make_propagator_fn(prop: Propagator, phys: PhysicsParams, n_steps: int):
     """(x, v) -> run(x, v, n_steps) for parareal."""
     return lambda u: run(u[0], u[1], n_steps, prop, phys)

@@ -21,6 +21,7 @@ lib = C.CDLL(_LIB_PATH)
 
 PIF_PROP_PIF_NUFFT = 0
 PIF_PROP_PIC_CIC = 1
+PIF_FLAG_FP32_ALLREDUCE = 1
 STATUS = {0: "PIF_OK", 1: "PIF_ERR_ARG", 2: "PIF_ERR_CONFIG", 3: "PIF_ERR_NUMERIC",
           4: "PIF_ERR_CUDA", 5: "PIF_ERR_NCCL", 6: "PIF_ERR_OOM", 7: "PIF_ERR_STATE"}
 
@@ -32,7 +33,7 @@ class PifPhysics(C.Structure):
 
 class PifPropagator(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("spline_order", C.c_int32),
-                ("tol", C.c_double), ("dt", C.c_double)]
+                ("flags", C.c_int32), ("tol", C.c_double), ("dt", C.c_double)]
 
 
 class PifDist(C.Structure):
@@ -73,6 +74,7 @@ _sig = {
     "pif_debug_type2": [_ctx, C.c_int, _dp, _dp, _i64, _dp],
     "pif_debug_push": [_ctx, C.c_int, _dp, _dp, _dp, _i64, C.c_int, C.c_int],
     "pif_profile": [_ctx, C.c_int],
+    "pif_get_rho": [_ctx, _dp],
     "pif_debug_parareal_protocol": [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p,
                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -123,11 +125,12 @@ def physics(L, q_over_m, total_charge, B=(0.0, 0.0, 0.0), A=(0.0,) * 9, c=(0.0, 
     return p
 
 
-def propagator(kind, n, dt, tol=1e-12, spline_order=1):
+def propagator(kind, n, dt, tol=1e-12, spline_order=1, fp32_allreduce=False):
     if isinstance(kind, str):
         kind = {"pif": PIF_PROP_PIF_NUFFT, "pic": PIF_PROP_PIC_CIC}[kind]
     p = PifPropagator()
     p.kind, p.n, p.spline_order, p.tol, p.dt = kind, n, spline_order, tol, dt
+    p.flags = PIF_FLAG_FP32_ALLREDUCE if fp32_allreduce else 0
     return p
 
 
@@ -219,6 +222,14 @@ def pif_parareal(ctx, t0, t1, n_slices, max_iter, stop_tol, n_blocks=1):
                 err_v=np.array(ev[:max_iter * n_slices]).reshape(shape),
                 t_coarse0=r.t_coarse0, t_fine=r.t_fine, t_coarse=r.t_coarse, t_comm=r.t_comm,
                 t_total=r.t_total)
+
+
+def pif_get_rho(ctx, N):
+    """rho_tilde on the Hermitian half box, complex array [N+1, N+1, N/2+1] indexed
+    [mx + N/2, my + N/2, mz]."""
+    out = np.empty(2 * (N + 1) ** 2 * (N // 2 + 1))
+    _check("pif_get_rho", lib.pif_get_rho(ctx, out.ctypes.data))
+    return out.view(np.complex128).reshape(N + 1, N + 1, N // 2 + 1)
 
 
 def pif_finalize(ctx):

@@ -149,7 +149,21 @@ __global__ void k_check_finite(const double* __restrict__ a, int64_t count, int*
     if (!isfinite(a[i])) atomicExch(flag, 1);
 }
 
+// fp64 <-> fp32 staging for the fp32 density all-reduce (PIF_FLAG_FP32_ALLREDUCE)
+__global__ void k_convert(double* __restrict__ d, float* __restrict__ f, int64_t count, int to_float) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (to_float) f[i] = (float)d[i];
+    else d[i] = (double)f[i];
+  }
+}
+
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_convert(double* d, float* f, int64_t count, bool to_float, cudaStream_t st) {
+  k_convert<<<kReduceBlocks, 256, 0, st>>>(d, f, count, to_float ? 1 : 0);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cic_deposit(const double* x, int64_t stride, int64_t n, int Ng, double inv_h,
                                double* grid, cudaStream_t st) {

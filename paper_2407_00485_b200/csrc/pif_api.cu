@@ -157,6 +157,8 @@ void horner_fit(int w, double beta, Horner& hc) {
 
 struct Plan {
   bool valid = false;
+  bool fp32_ar = false;  // PIF_FLAG_FP32_ALLREDUCE
+  void* ar32 = nullptr;  // fp32 staging buffer of the all-reduced density
   Horner hc{};
   int kind = 0, N = 0, order = 1;
   double tol = 0, dt = 0;
@@ -248,6 +250,8 @@ size_t layout(pif_ctx c, char* base) {
     p.spec = (double2*)take(p.spec_elems() * sizeof(double2));
     p.G3 = (double2*)take(3 * p.spec_elems() * sizeof(double2));
     p.grid3 = (double*)take(3 * p.grid_pts() * sizeof(double));
+    if (p.fp32_ar)
+      p.ar32 = take((p.kind == PIF_PROP_PIF_NUFFT ? 2 * p.box_elems() : p.grid_pts()) * sizeof(float));
     if (p.kind == PIF_PROP_PIF_NUFFT) {
       p.box = (double2*)take(p.box_elems() * sizeof(double2));
       p.cor = (double*)take((p.N + 1) * sizeof(double));
@@ -265,6 +269,7 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
   p.kind = pr->kind;
   p.N = pr->n;
   p.order = pr->spline_order;
+  p.fp32_ar = (pr->flags & PIF_FLAG_FP32_ALLREDUCE) != 0;
   p.tol = pr->tol;
   p.dt = pr->dt;
   const double L = c->ph.L;
@@ -416,6 +421,19 @@ pif_status sort_particles(pif_ctx c, Plan& p) {
   return PIF_OK;
 }
 
+// Sum the density buffer (count doubles) over the space group: fp64, or fp32
+// (PIF_FLAG_FP32_ALLREDUCE) through the plan's float staging buffer.
+pif_status density_allreduce(pif_ctx c, Plan& p, double* buf, int64_t count) {
+  if (!p.fp32_ar) {
+    NC(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm_space, c->st));
+    return PIF_OK;
+  }
+  CU(launch_convert(buf, (float*)p.ar32, count, true, c->st));
+  NC(ncclAllReduce(p.ar32, p.ar32, count, ncclFloat, ncclSum, c->comm_space, c->st));
+  CU(launch_convert(buf, (float*)p.ar32, count, false, c->st));
+  return PIF_OK;
+}
+
 // One field solve of plan `which` at the current positions followed by the
 // fused interpolation + push (kicks half kicks, optional drift).
 pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
@@ -432,8 +450,7 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     const double L = c->ph.L;
     PH(PH_BOX, CU(launch_extract_box(p.spec, p.n, p.N, p.cor, c->q / (L * L * L), p.box, c->st)));
     if (c->space_size > 1)
-      PH(PH_ALLREDUCE, NC(ncclAllReduce(p.box, p.box, 2 * p.box_elems(), ncclDouble, ncclSum,
-                                        c->comm_space, c->st)));
+      PH(PH_ALLREDUCE, TRY(density_allreduce(c, p, (double*)p.box, 2 * p.box_elems())));
     PH(PH_POISSON, CU(launch_poisson_pad(p.box, p.n, p.N, L, p.cor, p.S, p.G3, c->st)));
     PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
     PH(PH_INTERP_PUSH, CU(launch_interp_push(p.grid3, c->xA, c->vA, n, c->idA, nullptr,
@@ -448,8 +465,7 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
       CU(launch_cic_deposit(c->xA, n, n, Ng, 1.0 / h, p.grid, c->st));
     });
     if (c->space_size > 1)
-      PH(PH_ALLREDUCE, NC(ncclAllReduce(p.grid, p.grid, p.grid_pts(), ncclDouble, ncclSum,
-                                        c->comm_space, c->st)));
+      PH(PH_ALLREDUCE, TRY(density_allreduce(c, p, p.grid, p.grid_pts())));
     PH(PH_FFT_FWD, CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec)));
     double scale = c->q / (h * h * h) / (double)p.grid_pts();
     PH(PH_POISSON, CU(launch_pic_poisson(p.spec, Ng, c->ph.L, scale, p.G3, c->st)));
@@ -757,6 +773,18 @@ pif_status pif_field_energy(pif_ctx c, double W[3], double* kinetic, double mome
   return PIF_OK;
 }
 
+pif_status pif_get_rho(pif_ctx c, double* out) {
+  TRY(need_ready(c));
+  if (!out) return fail(PIF_ERR_ARG, "null argument");
+  Plan& p = c->plan[0];
+  if (p.kind != PIF_PROP_PIF_NUFFT) return fail(PIF_ERR_CONFIG, "fine propagator is not PIF");
+  TRY(materialize(c));
+  if (!c->box_fresh) TRY(solve_and_push(c, 0, 0, 0));
+  CU(cudaMemcpyAsync(out, p.box, p.box_elems() * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  return PIF_OK;
+}
+
 pif_status pif_plan_info(pif_ctx c, int which, int32_t* w, double* beta, int32_t* n_up) {
   if (!c || which < 0 || which > 1 || !c->plan[which].valid) return fail(PIF_ERR_ARG, "bad plan");
   const Plan& p = c->plan[which];
@@ -767,15 +795,9 @@ pif_status pif_plan_info(pif_ctx c, int which, int32_t* w, double* beta, int32_t
 }
 
 // ---------------------------------------------------------------- parareal --
-pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32_t max_iter,
-                        double stop_tol, int32_t n_blocks, pif_parareal_report* rep) {
-  TRY(need_ready(c));
-  if (!rep || !rep->retired_at || !rep->err_x || !rep->err_v) return fail(PIF_ERR_ARG, "null report");
-  if (!c->plan[1].valid) return fail(PIF_ERR_CONFIG, "parareal needs a coarse propagator");
-  if (n_slices < 1 || max_iter < 0 || !(t1 > t0)) return fail(PIF_ERR_ARG, "bad slices / iterations / interval");
-  if (n_blocks != 1) return fail(PIF_ERR_CONFIG, "n_blocks > 1 (windowed parareal) is not implemented");
-  if (c->time_size > 1 && n_slices != c->time_size)
-    return fail(PIF_ERR_CONFIG, "n_slices must equal the number of time ranks");
+// One parareal window [t0, t1] with n_slices slices (the body of pif_parareal).
+static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_slices,
+                                  int32_t max_iter, double stop_tol, pif_parareal_report* rep) {
   const double dT = (t1 - t0) / n_slices;
   const int64_t nf = llround(dT / c->plan[0].dt), ng = llround(dT / c->plan[1].dt);
   if (nf < 1 || ng < 1 || std::fabs(nf * c->plan[0].dt - dT) > 1e-9 * dT ||
@@ -1000,6 +1022,56 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
   rep->t_coarse = t_coarse;
   rep->t_comm = t_comm;
   rep->t_total = now() - tt0;
+  return PIF_OK;
+}
+
+pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32_t max_iter,
+                        double stop_tol, int32_t n_blocks, pif_parareal_report* rep) {
+  TRY(need_ready(c));
+  if (!rep || !rep->retired_at || !rep->err_x || !rep->err_v) return fail(PIF_ERR_ARG, "null report");
+  if (!c->plan[1].valid) return fail(PIF_ERR_CONFIG, "parareal needs a coarse propagator");
+  if (n_slices < 1 || max_iter < 0 || !(t1 > t0) || n_blocks < 1)
+    return fail(PIF_ERR_ARG, "bad slices / iterations / interval / blocks");
+  if (c->time_size > 1 && n_slices != c->time_size)
+    return fail(PIF_ERR_CONFIG, "n_slices must equal the number of time ranks");
+  // Multi-block parareal (reading R22): n_blocks equal windows solved
+  // one after the other, each by parareal with n_slices slices; the final state
+  // of a window (on the last time rank) seeds the next window on every rank.
+  const double W = (t1 - t0) / n_blocks;
+  int total_iter = 0, all_conv = 1;
+  double tf = 0, tg = 0, tg0 = 0, tc = 0, tt = 0;
+  for (int b = 0; b < n_blocks; ++b) {
+    TRY(parareal_window(c, t0 + b * W, (b + 1 == n_blocks) ? t1 : t0 + (b + 1) * W, n_slices,
+                        max_iter, stop_tol, rep));
+    total_iter += rep->iterations;
+    all_conv &= rep->converged;
+    tf += rep->t_fine;
+    tg += rep->t_coarse;
+    tg0 += rep->t_coarse0;
+    tc += rep->t_comm;
+    tt += rep->t_total;
+    if (c->time_size > 1 && b + 1 < n_blocks) {
+      // hand U_{n_slices} of this window from the last time rank to all time ranks
+      double t0c = now();
+      const int64_t n = c->nloc;
+      double* buf = nullptr;
+      CU(cudaMallocAsync((void**)&buf, 6 * n * sizeof(double), c->st));
+      if (c->t_idx == c->time_size - 1) TRY(store_state(c, buf));
+      NC(ncclBroadcast(buf, buf, 6 * n, ncclDouble, c->time_size - 1, c->comm_time, c->st));
+      TRY(load_state(c, buf));
+      CU(cudaFreeAsync(buf, c->st));
+      CU(cudaStreamSynchronize(c->st));
+      tc += now() - t0c;
+      tt += now() - t0c;
+    }
+  }
+  rep->iterations = total_iter;  // summed over windows; per-slice fields are the last window's
+  rep->converged = all_conv;
+  rep->t_fine = tf;
+  rep->t_coarse = tg;
+  rep->t_coarse0 = tg0;
+  rep->t_comm = tc;
+  rep->t_total = tt;
   return PIF_OK;
 }
 

@@ -175,6 +175,7 @@ cudaError_t launch_iota(int* id, int64_t n, cudaStream_t st);
 cudaError_t launch_correct_norms(const double* F, const double* Gn, const double* Go, double* U,
                                  int64_t n, double L, double* partials, double* out4,
                                  cudaStream_t st);
+cudaError_t launch_convert(double* d, float* f, int64_t count, bool to_float, cudaStream_t st);
 cudaError_t launch_check_finite(const double* a, int64_t count, int* flag, cudaStream_t st);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs

@@ -48,11 +48,12 @@ def gather_rows(t):
     return torch.cat([o[:, : int(v.item())] for o, v in zip(outs, ns)], dim=1)
 
 
-def run_space(rank, world, local, nid):
-    """Particle decomposition over all ranks: 20 fine steps == single GPU."""
+def run_space(rank, world, local, nid, fp32=False):
+    """Particle decomposition over all ranks: 20 fine steps == single GPU (fp32:
+    the rho_hat all-reduce in single precision)."""
     n, steps = 20000 + 3, 20  # ragged split
     x0, v0 = landau_state(n, 3)
-    fine = P.propagator("pif", 8, 0.05, tol=1e-12)
+    fine = P.propagator("pif", 8, 0.05, tol=1e-12, fp32_allreduce=fp32)
     sim = P.Simulation(phys(), fine, None, n_particles=n, device=local, rank=rank, world=world,
                        space_size=world, nccl_id=nid)
     a, c = sim.first, sim.n_local
@@ -65,7 +66,8 @@ def run_space(rank, world, local, nid):
     sim.close()
     res = {}
     if rank == 0:
-        ref = P.Simulation(phys(), fine, None, n_particles=n, device=local)
+        ref = P.Simulation(phys(), P.propagator("pif", 8, 0.05, tol=1e-12), None, n_particles=n,
+                           device=local)
         ref.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
         ref.step(steps)
         xr, vr = ref.get_state()
@@ -81,7 +83,7 @@ def run_space(rank, world, local, nid):
     return res
 
 
-def run_parareal(rank, world, local, nid, space_size):
+def run_parareal(rank, world, local, nid, space_size, blocks=1):
     """Pipelined parareal (time_size = world / space_size slices, one per time
     rank) == the serial-schedule parareal of the same problem on one GPU."""
     n = 4096 + 5
@@ -90,13 +92,13 @@ def run_parareal(rank, world, local, nid, space_size):
     nf, dtf, dtg = 4, 0.05, 0.1
     fine = P.propagator("pif", 8, dtf, tol=1e-12)
     coarse = P.propagator("pic", 8, dtg)
-    t1 = T * nf * dtf
+    t1 = blocks * T * nf * dtf
     sim = P.Simulation(phys(), fine, coarse, n_particles=n, device=local, rank=rank, world=world,
                        space_size=space_size, nccl_id=nid)
     a, c = sim.first, sim.n_local
     sim.set_state(torch.from_numpy(np.ascontiguousarray(x0[:, a:a + c])).cuda(),
                   torch.from_numpy(np.ascontiguousarray(v0[:, a:a + c])).cuda())
-    rep = sim.parareal(0.0, t1, T, T, 1e-6)
+    rep = sim.parareal(0.0, t1, T, T, 1e-6, n_blocks=blocks)
     x, v = sim.get_state()
     # final state lives on the last time rank: gather its space group's rows
     t_idx = rank // space_size
@@ -109,7 +111,7 @@ def run_parareal(rank, world, local, nid, space_size):
         xl, vl = xs[:, last], vs[:, last]
         ref = P.Simulation(phys(), fine, coarse, n_particles=n, device=local)
         ref.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
-        rr = ref.parareal(0.0, t1, T, T, 1e-6)
+        rr = ref.parareal(0.0, t1, T, T, 1e-6, n_blocks=blocks)
         xr, vr = ref.get_state()
         L = landau_physics().L
         dx = (xl - xr).cpu().numpy()
@@ -130,10 +132,14 @@ def main():
     rank, world, local, nid = setup()
     if mode == "space":
         res = run_space(rank, world, local, nid)
+    elif mode == "space32":
+        res = run_space(rank, world, local, nid, fp32=True)
     elif mode == "parareal":
         res = run_parareal(rank, world, local, nid, space_size=1)
     elif mode == "spacetime":
         res = run_parareal(rank, world, local, nid, space_size=2)
+    elif mode == "blocks":
+        res = run_parareal(rank, world, local, nid, space_size=1, blocks=3)
     else:
         raise SystemExit(mode)
     if rank == 0:

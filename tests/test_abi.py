@@ -49,7 +49,8 @@ def test_struct_layout_matches_c(L):
 int main(void) {
   printf("%zu %zu %zu %zu\n", sizeof(pif_physics), sizeof(pif_propagator), sizeof(pif_dist),
          sizeof(pif_parareal_report));
-  printf("%zu %zu %zu %zu %zu\n", offsetof(pif_propagator, tol), offsetof(pif_dist, nccl_id),
+  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(pif_propagator, tol), offsetof(pif_propagator, flags),
+         offsetof(pif_dist, nccl_id),
          offsetof(pif_parareal_report, retired_at), offsetof(pif_parareal_report, t_coarse0),
          offsetof(pif_physics, E_ext_c));
   return 0;
@@ -64,7 +65,7 @@ int main(void) {
     sizes = [int(v) for v in out]
     assert sizes[:4] == [ctypes.sizeof(L.PifPhysics), ctypes.sizeof(L.PifPropagator),
                          ctypes.sizeof(L.PifDist), ctypes.sizeof(L.PifPararealReport)]
-    assert sizes[4:] == [L.PifPropagator.tol.offset, L.PifDist.nccl_id.offset,
+    assert sizes[4:] == [L.PifPropagator.tol.offset, L.PifPropagator.flags.offset, L.PifDist.nccl_id.offset,
                          L.PifPararealReport.retired_at.offset,
                          L.PifPararealReport.t_coarse0.offset, L.PifPhysics.E_ext_c.offset]
 

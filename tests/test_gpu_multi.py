@@ -46,3 +46,18 @@ def test_spacetime_parareal_4gpu():
     r = launch(4, "spacetime", 29613)
     assert r["retired"] == r["retired_ref"] and r["iters"] == r["iters_ref"], r
     assert r["dx"] <= 1e-9 and r["dv"] <= 1e-9, r
+
+
+@pytest.mark.skipif(ngpu() < 2, reason="needs 2 GPUs")
+def test_space_decomposition_fp32_allreduce_2gpu():
+    """f3: rho_hat all-reduced in fp32: same trajectories to single-precision level."""
+    r = launch(2, "space32", 29614)
+    assert 0 < r["dx"] <= 1e-6 and r["dv"] <= 1e-5, r
+
+
+@pytest.mark.skipif(ngpu() < 2, reason="needs 2 GPUs")
+def test_multiblock_pipelined_parareal_2gpu():
+    """f1: 3 windows of pipelined parareal on 2 time ranks == serial schedule."""
+    r = launch(2, "blocks", 29615)
+    assert r["retired"] == r["retired_ref"] and r["iters"] == r["iters_ref"], r
+    assert r["dx"] <= 1e-9 and r["dv"] <= 1e-9, r

@@ -374,3 +374,24 @@ def test_cold_plasma_oscillation_closed_form():
     wd = math.acos(1 - (S * dt) ** 2 / 2) / dt
     t = dt * np.arange(1, nsteps + 1)
     assert np.max(np.abs(np.array(amp) - np.cos(wd * t))) < 2e-4
+
+
+def test_parareal_blocks_exact_and_linear():
+    """Multi-block parareal: (1) scalar linear propagators -- each window applies
+    the truncated binomial expansion to its seed, so after B windows the result is
+    (sum_{j<=K} C(Ns,j)(f-g)^j g^(Ns-j))^B u0; (2) tol = 0, K = N_s per window ->
+    serial fine over all windows."""
+    f, g, u0, Ns, B, K = 0.9, 0.8, 1.3, 3, 2, 1
+    F = lambda u: (u[0] * f, u[1] * f)
+    G = lambda u: (u[0] * g, u[1] * g)
+    res = O.parareal_blocks((np.array([u0]), np.array([u0])), lambda b: F, lambda b: G, Ns, B, K, -1.0)
+    per = sum(math.comb(Ns, j) * (f - g) ** j * g ** (Ns - j) for j in range(K + 1))
+    assert abs(res[-1].U[Ns][0][0] - per ** B * u0) < 1e-14
+    phys = O.PhysicsParams.from_inputs(landau_physics())
+    x, v = landau_state(64, 12)
+    Fp, Gp = O.Propagator("pif", 4, 0.05), O.Propagator("pic", 4, 0.1)
+    res = O.parareal_blocks((x, v), lambda b: O.make_propagator_fn(Fp, phys, 2),
+                            lambda b: O.make_propagator_fn(Gp, phys, 1), 2, 3, 2, 0.0, L=phys.L)
+    xs, vs = O.run(x, v, 2 * 2 * 3, Fp, phys)
+    assert np.abs(O.min_image(res[-1].U[2][0] - xs, phys.L)).max() < 1e-12 * phys.L
+    assert np.abs(res[-1].U[2][1] - vs).max() < 1e-12
