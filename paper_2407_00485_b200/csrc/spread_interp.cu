@@ -318,7 +318,8 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
   // g tile -> B fragments: gB[ks][nt][d][l] = g_d[c = 4 ks + (l & 3)][z = 8 nt + (l >> 2)]
   // (consecutive threads read consecutive z of one column: coalesced)
   {
-    // one (component, column) pair per 16 lanes: each lane one z of the column
+    // g tile -> smem B fragments with cp.async (overlaps the first chunk's
+    // staging); one (component, column) pair per ZP lanes, one z per lane
     constexpr int ZP = C::NT * 8;           // padded z extent (8 or 16)
     constexpr int PER = 32 / ZP;            // (d, c) pairs per warp step
     const int zl = lane % ZP, sub = lane / ZP;
@@ -330,22 +331,27 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
       int gx = T0[0] + cx, gy = T0[1] + cy;
       gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
       gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
-      const double val = zl < RZ ? grid3[d * n3 + ((int64_t)gx * n + gy) * n + gz] : 0.0;
-      S.gB[c >> 2][zl >> 3][d][((zl & 7) << 2) | (c & 3)] = val;
+      double* dst = &S.gB[c >> 2][zl >> 3][d][((zl & 7) << 2) | (c & 3)];
+      if (zl < RZ) cp_async8(dst, grid3 + d * n3 + ((int64_t)gx * n + gy) * n + gz);
+      else *dst = 0.0;
     }
+    cp_async_commit();
   }
 
   int buf = 0;
   for (int64_t base = start; base < end; base += kIChunk, buf ^= 1) {
     const int cnt = (int)min((int64_t)kIChunk, end - base);
     const int pad = (cnt + 7) & ~7;
-    cp_async_wait_all();
+    // chunk 0: x/v (group 0) may land before the g tile (group 1)
+    if (base == start) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else cp_async_wait_all();
     __syncthreads();  // every thread's cp.async data for this chunk is visible
     for (int q = tid; q < cnt; q += blockDim.x) {
       const double xr[3] = {S.xv[buf][0][q], S.xv[buf][1][q], S.xv[buf][2][q]};
       stage_position(sm, q, xr, g, T0);
     }
-    stage_psi<true>(sm, cnt, pad, g, T0, hc);  // its barriers also publish gB
+    if (base == start) cp_async_wait_all();  // g tile landed (published by stage_psi's barriers)
+    stage_psi<true>(sm, cnt, pad, g, T0, hc);
     if (base + kIChunk < end) prefetch(buf ^ 1, base + kIChunk, (int)min((int64_t)kIChunk, end - base - kIChunk));
     for (int p0 = 8 * wid; p0 < pad; p0 += 8 * C::NW) {
       const int pa = p0 + gr;  // A row (particle) of this lane
@@ -354,10 +360,15 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
         for (int d = 0; d < 3; ++d) acc[nt][d][0] = acc[nt][d][1] = 0.0;
+      int cx = tq % RX, cy = tq / RX;  // column c = 4 ks + tq, advanced incrementally
 #pragma unroll 4
       for (int ks = 0; ks < C::KS; ++ks) {
-        const int c = 4 * ks + tq;
-        const double a = sm.px[pa][c % RX] * sm.py[pa][c / RX];  // A[g][t] = W[p0+g][4ks+t]
+        const double a = sm.px[pa][cx] * sm.py[pa][cy];  // A[g][t] = W[p0+g][4ks+t]
+        cx += 4;
+        if (cx >= RX) {
+          cx -= RX;
+          cy += 1;
+        }
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
