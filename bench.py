@@ -28,11 +28,15 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = 1  # BASELINE.json configs[1]
+CFG = 1  # BASELINE.json configs[1] (the default workload); --config 2/3 for C3/C4 lines
 N_MODES = 32
 N_PER_GPU = 1 << 21
 TOL = 1e-12
 DT = 0.05
+CASE = "landau"
+CONFIGS = {1: ("landau", 32, 1 << 21, 1e-12, 0.05),     # C2
+           2: ("tsi", 32, 1 << 23, 1e-12, 0.05),        # C3
+           3: ("penning", 64, 1 << 24, 1e-12, 0.003125)}  # C4 (Boris push)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 SM_COUNT = 148
@@ -47,7 +51,13 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS),
+                    help="BASELINE.json configs index (default 1 = the headline workload)")
+    args = ap.parse_args()
+    global CFG, CASE, N_MODES, N_PER_GPU, TOL, DT
+    CFG = args.config
+    CASE, N_MODES, N_PER_GPU, TOL, DT = CONFIGS[CFG]
+    return args
 
 
 def env_dist():
@@ -108,10 +118,10 @@ def oracle_step_rate(n_sample, seed=CFG):
     import numpy as np
 
     import oracle as O
-    from pif_inputs import landau_physics, landau_state
+    from pif_inputs import make_case
 
-    ph = O.PhysicsParams.from_inputs(landau_physics())
-    x, v = landau_state(n_sample, seed)
+    p, x, v = make_case(CASE, n_sample, seed)
+    ph = O.PhysicsParams.from_inputs(p)
     prop = O.Propagator("pif", N_MODES, DT)
     E = np.zeros_like(x)  # E(x_n) carried from the previous step
     t0 = time.perf_counter()
@@ -129,14 +139,14 @@ def oracle_step_rate(n_sample, seed=CFG):
 
 
 def workload_name():
-    return f"landau_3d3v_{N_MODES}^3modes_{N_PER_GPU}particles_per_gpu_tol{TOL:g}_dt{DT}"
+    return f"{CASE}_3d3v_{N_MODES}^3modes_{N_PER_GPU}particles_per_gpu_tol{TOL:g}_dt{DT}"
 
 
 # ------------------------------------------------------------- reference --
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    n_sample = 1 << 15
+    n_sample = (1 << 15) * 32 ** 3 // N_MODES ** 3  # ~3 s of NUDFT per step
     rates, secs = [], []
     for i in range(args.warmup + args.steps):
         r, s, threads = oracle_step_rate(n_sample, seed=CFG + i)
@@ -152,7 +162,7 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(), "sample_particles": n_sample},
         "cpu_baseline": {"value": value, "unit": "particles/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{n_sample} of the {N_PER_GPU} Landau particles per step, one "
+                         "sample": f"{n_sample} of the {N_PER_GPU} {CASE} particles per step, one "
                                    f"KDK step of the exact O(N_p N^3) NUDFT PIF at N={N_MODES}"},
         "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -166,7 +176,7 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
 
     import paper_2407_00485_b200 as P
-    from pif_inputs import landau_physics, landau_state
+    from pif_inputs import make_case
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -177,15 +187,14 @@ def run_ours(args, rank, world, local):
         obj = [P.pif_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    p = landau_physics()
+    p, x0, v0 = make_case(CASE, N_PER_GPU, CFG + 1000 * rank)
     n_global = N_PER_GPU * world
     stream = torch.cuda.current_stream(dev)
-    sim = P.Simulation(P.physics(p.L, p.q_over_m, p.total_charge),
+    sim = P.Simulation(P.physics(p.L, p.q_over_m, p.total_charge, p.B, p.A, p.c),
                        P.propagator("pif", N_MODES, DT, tol=TOL), None, n_particles=n_global,
                        device=local, rank=rank, world=world, space_size=world, nccl_id=nccl_id,
                        stream=stream)
     w, beta, n_up = sim.plan_info(0)
-    x0, v0 = landau_state(sim.n_local, seed=CFG + 1000 * rank)
     xd = torch.from_numpy(x0).to(dev)
     vd = torch.from_numpy(v0).to(dev)
     sim.set_state(xd, vd)
@@ -265,10 +274,10 @@ def run_ours(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_sample = 1 << 17
-        rate, secs, threads = oracle_step_rate(n_sample)
+        n_sample = (1 << 17) * 32 ** 3 // N_MODES ** 3  # ~10-30 s of NUDFT work
+        rate, secs, threads = oracle_step_rate(n_sample, seed=CFG)
         cpu = {"value": rate, "unit": "particles/s", "cores": threads, "kind": "oracle",
-               "sample": f"{n_sample} of the {N_PER_GPU} configs[1] Landau particles, one KDK "
+               "sample": f"{n_sample} of the {N_PER_GPU} configs[{CFG}] {CASE} particles, one KDK "
                          f"step of the exact O(N_p N^3) NUDFT PIF at N={N_MODES} ({secs:.1f} s)"}
     sim.close()
     if rank == 0:

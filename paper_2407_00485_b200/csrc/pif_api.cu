@@ -201,7 +201,9 @@ struct pif_ctx_s {
   size_t ws_bytes = 0;
   double *xA = nullptr, *vA = nullptr, *xB = nullptr, *vB = nullptr;
   int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *counts = nullptr,
-      *offsets = nullptr, *flag = nullptr;
+      *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr;
+  int4 *sitems = nullptr, *iitems = nullptr;
+  int64_t max_s = 1, max_i = 1;
   double *partials = nullptr, *red = nullptr;
   void* fft_work = nullptr;
   int64_t max_bins = 1;
@@ -238,6 +240,18 @@ size_t layout(pif_ctx c, char* base) {
   c->rnk = (int*)take(n * sizeof(int));
   c->counts = (int*)take(c->max_bins * sizeof(int));
   c->offsets = (int*)take((c->max_bins + 1) * sizeof(int));
+  c->soff = (int*)take((c->max_bins + 1) * sizeof(int));
+  c->ioff = (int*)take((c->max_bins + 1) * sizeof(int));
+  c->max_s = c->max_i = 1;
+  for (int i = 0; i < 2; ++i) {
+    const Plan& p = c->plan[i];
+    if (!p.valid || p.kind != PIF_PROP_PIF_NUFFT) continue;
+    const int64_t M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
+    c->max_s = std::max(c->max_s, sched_max_s(p.nbricks, M, n));
+    c->max_i = std::max(c->max_i, sched_max_i(p.nbricks, n));
+  }
+  c->sitems = (int4*)take(c->max_s * sizeof(int4));
+  c->iitems = (int4*)take(c->max_i * sizeof(int4));
   c->flag = (int*)take(64);
   c->partials = (double*)take(4 * kReduceBlocks * sizeof(double));
   c->red = (double*)take(16 * sizeof(double));
@@ -285,7 +299,12 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     int RI[3], m[3] = {1, 1, 1};
     if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
     else if (w <= 9) { RI[0] = RI[1] = RI[2] = 12; }
-    else if (w == 13) { RI[0] = 14; RI[1] = 14; RI[2] = 16; m[0] = m[1] = 2; }
+#ifndef PIF_W13_TILE
+#define PIF_W13_TILE 1
+#endif
+    else if (w == 13 && PIF_W13_TILE == 1) { RI[0] = 14; RI[1] = 14; RI[2] = 16; m[0] = m[1] = 2; }
+    else if (w == 13 && PIF_W13_TILE == 2) { RI[0] = 16; RI[1] = 14; RI[2] = 16; m[1] = 2; }
+    else if (w == 13 && PIF_W13_TILE == 3) { RI[0] = RI[1] = RI[2] = 16; }
     else { RI[0] = RI[1] = RI[2] = 16; }
     Brick& g = p.g;
     g.n = n;
@@ -407,12 +426,18 @@ pif_status ph_mark(pif_ctx c, int ph) {
     TRY(ph_mark(c, ph));        \
   } while (0)
 
+Sched sched_of(pif_ctx c, const Plan& p) {
+  const int64_t M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
+  return Sched{c->offsets, c->soff, c->ioff, c->sitems, c->iitems, p.nbricks,
+               sched_max_s(p.nbricks, M, c->nloc), sched_max_i(p.nbricks, c->nloc)};
+}
+
 // a0: counting sort of the working particles (xA, vA, idA) by brick of plan p.
 pif_status sort_particles(pif_ctx c, Plan& p) {
   const int64_t n = c->nloc;
   CU(cudaMemsetAsync(c->counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(c->xA, n, n, p.g, c->key, c->rnk, c->counts, c->st));
-  CU(launch_scan(c->counts, c->offsets, p.nbricks, c->st));
+  CU(launch_schedule(c->counts, sched_of(c, p), p.g.m[0] * p.g.m[1] * p.g.m[2], c->st));
   CU(launch_scatter_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->xB,
                            c->vB, c->idB, nullptr, c->st));
   std::swap(c->xA, c->xB);
@@ -444,7 +469,7 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_SORT, TRY(sort_particles(c, p)));
     PH(PH_SPREAD, {
       CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-      CU(launch_spread(c->xA, n, nullptr, 1.0, c->offsets, p.g, p.hc, p.grid, c->st));
+      CU(launch_spread(c->xA, n, nullptr, 1.0, sched_of(c, p), p.g, p.hc, p.grid, c->st));
     });
     PH(PH_FFT_FWD, CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec)));
     const double L = c->ph.L;
@@ -454,7 +479,7 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_POISSON, CU(launch_poisson_pad(p.box, p.n, p.N, L, p.cor, p.S, p.G3, c->st)));
     PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
     PH(PH_INTERP_PUSH, CU(launch_interp_push(p.grid3, c->xA, c->vA, n, c->idA, nullptr,
-                                             c->offsets, p.g, p.hc, P, c->st)));
+                                             sched_of(c, p), p.g, p.hc, P, c->st)));
     c->launches += 7;  // bin, scan, scatter, spread, extract, poisson, interp_push
     c->box_fresh = (which == 0) && !drift;
   } else {
@@ -1124,6 +1149,19 @@ pif_status pif_finalize(pif_ctx c) {
 }
 
 // ------------------------------------------------------------- debug/tests --
+// Temporary schedule for the debug transforms (one cudaMalloc: counts + Sched).
+static pif_status debug_sched(pif_ctx c, const Plan& p, int64_t n, int** counts, Sched& S) {
+  const int64_t K = p.nbricks, M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
+  const int64_t ms = sched_max_s(K, M, n), mi = sched_max_i(K, n);
+  const size_t ints = K + 3 * (K + 1);
+  char* buf = nullptr;
+  CU(cudaMalloc(&buf, ints * sizeof(int) + 16 + (ms + mi) * sizeof(int4)));
+  int* ib = (int*)buf;
+  *counts = ib;
+  int4* items = (int4*)(((uintptr_t)(ib + ints) + 15) & ~(uintptr_t)15);
+  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, items, items + ms, K, ms, mi};
+  return PIF_OK;
+}
 pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, const double* s,
                            double* out) {
   if (!c || !x || !s || !out || n < 1) return fail(PIF_ERR_ARG, "null argument / empty input");
@@ -1143,18 +1181,19 @@ pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, con
   id2 = id + n;
   key = id + 2 * n;
   rk = id + 3 * n;
-  CU(cudaMalloc(&counts, (2 * p.nbricks + 1) * sizeof(int)));
-  offs = counts + p.nbricks;
+  Sched S;
+  TRY(debug_sched(c, p, n, &counts, S));
+  offs = S.offsets;
   CU(cudaMalloc(&dout, N3 * sizeof(double2)));
   CU(cudaMemcpyAsync(dx, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
   CU(cudaMemcpyAsync(ds, s, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
   CU(launch_iota(id, n, c->st));
   CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_scan(counts, offs, p.nbricks, c->st));
+  CU(launch_schedule(counts, S, p.g.m[0] * p.g.m[1] * p.g.m[2], c->st));
   CU(launch_scatter_sorted(dx, nullptr, id, ds, n, n, key, rk, offs, dx2, nullptr, id2, ds2, c->st));
   CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-  CU(launch_spread(dx2, n, ds2, 1.0, offs, p.g, p.hc, p.grid, c->st));
+  CU(launch_spread(dx2, n, ds2, 1.0, S, p.g, p.hc, p.grid, c->st));
   CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec));
   CU(launch_debug_extract_KN(p.spec, p.n, p.N, p.cor, dout, c->st));
   CU(cudaMemcpyAsync(out, dout, N3 * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
@@ -1181,20 +1220,21 @@ pif_status pif_debug_type2(pif_ctx c, int which, const double* cin, const double
   id2 = id + n;
   key = id + 2 * n;
   rk = id + 3 * n;
-  CU(cudaMalloc(&counts, (2 * p.nbricks + 1) * sizeof(int)));
-  offs = counts + p.nbricks;
+  Sched S;
+  TRY(debug_sched(c, p, n, &counts, S));
+  offs = S.offsets;
   CU(cudaMalloc(&dc, N3 * sizeof(double2)));
   CU(cudaMemcpyAsync(dx, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
   CU(cudaMemcpyAsync(dc, cin, N3 * sizeof(double2), cudaMemcpyHostToDevice, c->st));
   CU(launch_iota(id, n, c->st));
   CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_scan(counts, offs, p.nbricks, c->st));
+  CU(launch_schedule(counts, S, p.g.m[0] * p.g.m[1] * p.g.m[2], c->st));
   CU(launch_scatter_sorted(dx, nullptr, id, nullptr, n, n, key, rk, offs, dx2, nullptr, id2, nullptr, c->st));
   CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, c->st));
   CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3));
   PushArgs P = push_args(c, p, 0, 0);
-  CU(launch_interp_push(p.grid3, dx2, nullptr, n, id2, E, offs, p.g, p.hc, P, c->st));
+  CU(launch_interp_push(p.grid3, dx2, nullptr, n, id2, E, S, p.g, p.hc, P, c->st));
   CU(cudaMemcpyAsync(out, E, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CU(cudaStreamSynchronize(c->st));
   cudaFree(dx); cudaFree(dx2); cudaFree(E); cudaFree(id); cudaFree(counts); cudaFree(dc);

@@ -131,20 +131,40 @@ __device__ __forceinline__ void push_particle(double& x0, double& x1, double& x2
   }
 }
 
+// Per-step work schedule of the brick kernels: particle ranges of the sorted
+// arrays (offsets over sub-brick keys) cut into work items of at most kSpreadItem
+// (spread, per brick) / kInterpItem (interp, per sub-brick) particles, so a
+// crowded brick (e.g. the Penning cloud) is shared by several CTAs.  Item =
+// {brick or key, start, end, 0}; *_off are exclusive prefix sums over keys
+// (spread items attributed to the first key of their brick); totals at [nkeys].
+constexpr int kSpreadItem = 4096;
+constexpr int kInterpItem = 1024;
+struct Sched {
+  int* offsets;  // [nkeys + 1]
+  int* soff;     // [nkeys + 1]
+  int* ioff;     // [nkeys + 1]
+  int4* sitems;  // [max_s]
+  int4* iitems;  // [max_i]
+  int64_t nkeys, max_s, max_i;
+};
+inline int64_t sched_max_s(int64_t nkeys, int64_t M, int64_t n) { return nkeys / M + n / kSpreadItem + 1; }
+inline int64_t sched_max_i(int64_t nkeys, int64_t n) { return nkeys + n / kInterpItem + 1; }
+
 // -------------------------------------------------------------- launchers --
 // All launchers enqueue on `st` and return cudaGetLastError().
 cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const Brick& g, int* key,
                              int* rank, int* counts, cudaStream_t st);
 cudaError_t launch_scan(const int* counts, int* offsets, int64_t nbins, cudaStream_t st);
+cudaError_t launch_schedule(const int* counts, const Sched& S, int M, cudaStream_t st);
 cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,
                                   int64_t stride, int64_t n, const int* key, const int* rank,
                                   const int* offsets, double* x2, double* v2, int* id2, double* s2,
                                   cudaStream_t st);
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const int* offsets, const Brick& g, const Horner& hc, double* grid,
+                          const Sched& S, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st);
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
-                               const int* id, double* Eout, const int* offsets, const Brick& g,
+                               const int* id, double* Eout, const Sched& S, const Brick& g,
                                const Horner& hc, const PushArgs& P, cudaStream_t st);
 cudaError_t launch_extract_box(const double2* spec, int n, int N, const double* cor, double scale,
                                double2* box, cudaStream_t st);

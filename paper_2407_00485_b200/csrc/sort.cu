@@ -21,7 +21,16 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
   int k = ((B[0] * g.NB[1] + B[1]) * g.NB[2] + B[2]) * (g.m[0] * g.m[1] * g.m[2]) +
           (S[0] * g.m[1] + S[1]) * g.m[2] + S[2];
   key[j] = k;
-  rank[j] = atomicAdd(&counts[k], 1);
+  // warp-aggregated rank: one atomic per distinct key in the warp (sorted-ish
+  // input and crowded bricks give many equal keys per warp)
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, k);
+  const int leader = __ffs(peers) - 1;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&counts[k], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  rank[j] = base + __popc(peers & ((1u << lane) - 1u));
 }
 
 // Exclusive scan of counts[0..nbins) into offsets[0..nbins] with one CTA of
@@ -60,6 +69,93 @@ __global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ counts,
     excl += counts[i];
   }
   if (t == T - 1) offsets[nbins] = excl;
+}
+
+// Exclusive scans of (counts, spread items, interp items) over keys in one CTA;
+// per-thread chunks are whole bricks (multiples of M keys).
+__global__ void __launch_bounds__(1024) k_schedule_scan(const int* __restrict__ counts, Sched S,
+                                                        int M) {
+  __shared__ int sh[3][32];
+  const int T = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t nk = S.nkeys;
+  int64_t per = (nk + T - 1) / T;
+  per = (per + M - 1) / M * M;
+  const int64_t lo = min(nk, t * per), hi = min(nk, lo + per);
+  int a[3] = {0, 0, 0};
+  for (int64_t i = lo; i < hi; i += M) {
+    int bs = 0;
+    for (int m = 0; m < M; ++m) {
+      int c = counts[i + m];
+      a[0] += c;
+      a[2] += (c + kInterpItem - 1) / kInterpItem;
+      bs += c;
+    }
+    a[1] += (bs + kSpreadItem - 1) / kSpreadItem;
+  }
+  int incl[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int v = a[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    incl[q] = v;
+    if (lane == 31) sh[q][wid] = v;
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      int w = lane < (T >> 5) ? sh[q][lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int u = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += u;
+      }
+      sh[q][lane] = w;
+    }
+  }
+  __syncthreads();
+  int ex[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) ex[q] = incl[q] - a[q] + (wid > 0 ? sh[q][wid - 1] : 0);
+  for (int64_t i = lo; i < hi; i += M) {
+    int bs = 0;
+    for (int m = 0; m < M; ++m) bs += counts[i + m];
+    S.soff[i] = ex[1];
+    ex[1] += (bs + kSpreadItem - 1) / kSpreadItem;
+    for (int m = 0; m < M; ++m) {
+      int c = counts[i + m];
+      S.offsets[i + m] = ex[0];
+      S.ioff[i + m] = ex[2];
+      if (m) S.soff[i + m] = ex[1];
+      ex[0] += c;
+      ex[2] += (c + kInterpItem - 1) / kInterpItem;
+    }
+  }
+  if (t == T - 1) {
+    S.offsets[nk] = ex[0];
+    S.soff[nk] = ex[1];
+    S.ioff[nk] = ex[2];
+  }
+}
+
+// One thread per key: write the interp items of the key, and (first key of a
+// brick) the spread items of the brick.
+__global__ void k_schedule_fill(Sched S, int M) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= S.nkeys) return;
+  const int a = S.offsets[k], b = S.offsets[k + 1];
+  int it = S.ioff[k];
+  for (int s0 = a; s0 < b; s0 += kInterpItem) S.iitems[it++] = make_int4((int)k, s0, min(b, s0 + kInterpItem), 0);
+  if (k % M == 0) {
+    const int e = S.offsets[k + M];
+    int si = S.soff[k];
+    for (int s0 = a; s0 < e; s0 += kSpreadItem)
+      S.sitems[si++] = make_int4((int)(k / M), s0, min(e, s0 + kSpreadItem), 0);
+  }
 }
 
 __global__ void k_scatter_sorted(const double* __restrict__ x, const double* __restrict__ v,
@@ -108,6 +204,11 @@ cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const B
 }
 cudaError_t launch_scan(const int* counts, int* offsets, int64_t nbins, cudaStream_t st) {
   k_scan<<<1, 1024, 0, st>>>(counts, offsets, nbins);
+  return cudaGetLastError();
+}
+cudaError_t launch_schedule(const int* counts, const Sched& S, int M, cudaStream_t st) {
+  k_schedule_scan<<<1, 1024, 0, st>>>(counts, S, M);
+  k_schedule_fill<<<nblk(S.nkeys, 256), 256, 0, st>>>(S, M);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,

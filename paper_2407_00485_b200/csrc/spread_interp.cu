@@ -77,29 +77,30 @@ struct Psi {
   double str[CH];
 };
 
-// Decode a spread brick (sub == false) or interpolation sub-brick (sub == true)
-// from the CTA index into its tile origin T0 (grid points) and particle range.
-__device__ __forceinline__ void tile_of(const Brick& g, int cta, bool sub, int T0[3],
-                                        const int* __restrict__ offsets, int64_t& start,
-                                        int64_t& end) {
+// Decode a work item: spread (sub == false) = {brick, start, end}; interpolation
+// (sub == true) = {sub-brick key, start, end}; returns false past the last item.
+__device__ __forceinline__ bool tile_of(const Brick& g, const Sched& S, bool sub, int T0[3],
+                                        int64_t& start, int64_t& end) {
+  const int64_t item = blockIdx.x;
+  const int total = sub ? S.ioff[S.nkeys] : S.soff[S.nkeys];
+  if (item >= total) return false;
+  const int4 it = sub ? S.iitems[item] : S.sitems[item];
+  start = it.y;
+  end = it.z;
   const int M = g.m[0] * g.m[1] * g.m[2];
-  int brick = sub ? cta / M : cta;
+  const int brick = sub ? it.x / M : it.x;
   int bz = brick % g.NB[2], by = (brick / g.NB[2]) % g.NB[1], bx = brick / (g.NB[2] * g.NB[1]);
   T0[0] = bx * g.sb[0] - g.hw;
   T0[1] = by * g.sb[1] - g.hw;
   T0[2] = bz * g.sb[2] - g.hw;
   if (sub) {
-    int s = cta % M;
-    int sz = s % g.m[2], sy = (s / g.m[2]) % g.m[1], sx = s / (g.m[2] * g.m[1]);
+    int sk = it.x % M;
+    int sz = sk % g.m[2], sy = (sk / g.m[2]) % g.m[1], sx = sk / (g.m[2] * g.m[1]);
     T0[0] += sx * g.ib[0];
     T0[1] += sy * g.ib[1];
     T0[2] += sz * g.ib[2];
-    start = offsets[cta];
-    end = offsets[cta + 1];
-  } else {
-    start = offsets[brick * M];
-    end = offsets[(brick + 1) * M];
   }
+  return start < end;
 }
 
 // Thread tid < cnt: record particle tid's grid coordinate and window offset.
@@ -185,15 +186,14 @@ struct SpreadCfg {
 template <int RX, int RY, int RZ, bool HAS_S>
 __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
     k_spread(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
-             double s_uniform, const int* __restrict__ offsets, Brick g,
+             double s_uniform, const Sched Sc, Brick g,
              const __grid_constant__ Horner hc, double* __restrict__ grid) {
   using C = SpreadCfg<RX, RY, RZ>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Psi<RX, RY, RZ>& sm = *reinterpret_cast<Psi<RX, RY, RZ>*>(smem_raw);
   int T0[3];
   int64_t start, end;
-  tile_of(g, blockIdx.x, false, T0, offsets, start, end);
-  if (start == end) return;
+  if (!tile_of(g, Sc, false, T0, start, end)) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gr = lane >> 2, tq = lane & 3;
   // A-fragment rows: column c = (wid*CT + ct)*8 + gr
@@ -286,7 +286,7 @@ template <int RX, int RY, int RZ>
 __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
     k_interp_push(const double* __restrict__ grid3, double* __restrict__ x,
                   double* __restrict__ v, int64_t stride, const int* __restrict__ id,
-                  double* __restrict__ Eout, const int* __restrict__ offsets, Brick g,
+                  double* __restrict__ Eout, const Sched Sc, Brick g,
                   const __grid_constant__ Horner hc, PushArgs P) {
   using C = InterpCfg<RX, RY, RZ>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -294,8 +294,7 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
   Psi<RX, RY, RZ, kIChunk>& sm = S.psi;
   int T0[3];
   int64_t start, end;
-  tile_of(g, blockIdx.x, true, T0, offsets, start, end);
-  if (start == end) return;
+  if (!tile_of(g, Sc, true, T0, start, end)) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gr = lane >> 2, tq = lane & 3;
   const int n = g.n;
@@ -416,7 +415,7 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
 
 template <int A, int B, int Cz>
 static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, const double* s,
-                                 double s_uniform, const int* offsets, const Brick& g,
+                                 double s_uniform, const Sched& offsets, const Brick& g,
                                  const Horner& hc, double* grid, cudaStream_t st) {
   const int T = 32 * SpreadCfg<A, B, Cz>::NW;
   const size_t smem = sizeof(Psi<A, B, Cz, kChunk>);
@@ -438,9 +437,9 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
 }
 
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const int* offsets, const Brick& g, const Horner& hc, double* grid,
+                          const Sched& offsets, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st) {
-  const unsigned nbr = (unsigned)((int64_t)g.NB[0] * g.NB[1] * g.NB[2]);
+  const unsigned nbr = (unsigned)offsets.max_s;  // upper bound on spread items
 #define PIF_SPREAD(A, B, Cz)                                        \
   if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz)                \
     return spread_launch<A, B, Cz>(nbr, x, stride, s, s_uniform, offsets, g, hc, grid, st);
@@ -453,7 +452,7 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
 
 template <int A, int B, int Cz>
 static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, double* v,
-                                 int64_t stride, const int* id, double* Eout, const int* offsets,
+                                 int64_t stride, const int* id, double* Eout, const Sched& offsets,
                                  const Brick& g, const Horner& hc, const PushArgs& P,
                                  cudaStream_t st) {
   const int T = 32 * InterpCfg<A, B, Cz>::NW;
@@ -470,15 +469,16 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
 }
 
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
-                               const int* id, double* Eout, const int* offsets, const Brick& g,
+                               const int* id, double* Eout, const Sched& offsets, const Brick& g,
                                const Horner& hc, const PushArgs& P, cudaStream_t st) {
-  const unsigned nsub = (unsigned)g.nkeys;
+  const unsigned nsub = (unsigned)offsets.max_i;  // upper bound on interp items
 #define PIF_INTERP(A, B, Cz)                                                                   \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
   PIF_INTERP(8, 8, 8)
   PIF_INTERP(12, 12, 12)
   PIF_INTERP(14, 14, 16)
+  PIF_INTERP(16, 14, 16)
   PIF_INTERP(16, 16, 16)
 #undef PIF_INTERP
   return cudaErrorInvalidValue;
