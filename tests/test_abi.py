@@ -15,9 +15,9 @@ HEADER = os.path.join(ROOT, "include", "pif.h")
 
 @pytest.fixture(scope="module")
 def L():
-    from paper_2407_00485_b200 import _build
+    import __graft_entry__
 
-    _build.build()
+    __graft_entry__._build_module().build()
     from paper_2407_00485_b200 import _lib
 
     return _lib

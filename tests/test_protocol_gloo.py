@@ -65,8 +65,8 @@ def _worker(rank, world, port, max_iter, tol, out):
 def _worker_body(rank, world, port, max_iter, tol, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2407_00485_b200 import _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     from paper_2407_00485_b200 import _lib as L
     ph, x0, v0, F, G = problem()
     n = x0.shape[1]
@@ -119,8 +119,8 @@ def _worker_body(rank, world, port, max_iter, tol, out):
 
 @pytest.mark.parametrize("world,tol", [(2, 1e-6), (4, 1e-6), (4, 0.0)])
 def test_pipelined_protocol_equals_serial_parareal(world, tol):
-    from paper_2407_00485_b200 import _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     max_iter = world
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
