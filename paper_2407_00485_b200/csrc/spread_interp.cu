@@ -271,6 +271,10 @@ struct InterpCfg {
 #ifndef PIF_INW
 #define PIF_INW 8
 #endif
+#ifndef PIF_IMT
+#define PIF_IMT 1
+#endif
+  static constexpr int MT = PIF_IMT;  // m-tiles per warp pass (B-fragment reuse)
   static constexpr int NW = PIF_INW;       // warps (m-tiles processed round-robin)
   static_assert(NC % 4 == 0, "tile columns must be a multiple of 4");
 };
@@ -352,17 +356,24 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
     if (base == start) cp_async_wait_all();  // g tile landed (published by stage_psi's barriers)
     stage_psi<true>(sm, cnt, pad, g, T0, hc);
     if (base + kIChunk < end) prefetch(buf ^ 1, base + kIChunk, (int)min((int64_t)kIChunk, end - base - kIChunk));
-    for (int p0 = 8 * wid; p0 < pad; p0 += 8 * C::NW) {
-      const int pa = p0 + gr;  // A row (particle) of this lane
-      double acc[C::NT][3][2];
+    // each warp takes C::MT m-tiles of 8 particles at once: every smem B fragment feeds C::MT DMMAs
+    for (int p0 = 8 * C::MT * wid; p0 < pad; p0 += 8 * C::MT * C::NW) {
+      double acc[C::MT][C::NT][3][2];
 #pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt)
+      for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) acc[nt][d][0] = acc[nt][d][1] = 0.0;
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) acc[mt][nt][d][0] = acc[mt][nt][d][1] = 0.0;
       int cx = tq % RX, cy = tq / RX;  // column c = 4 ks + tq, advanced incrementally
-#pragma unroll 4
+#pragma unroll 2
       for (int ks = 0; ks < C::KS; ++ks) {
-        const double a = sm.px[pa][cx] * sm.py[pa][cy];  // A[g][t] = W[p0+g][4ks+t]
+        double a[C::MT];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) {
+          const int pa = min(p0 + 8 * mt + gr, kIChunk - 1);  // rows >= pad hold zero psi
+          a[mt] = sm.px[pa][cx] * sm.py[pa][cy];  // A[g][t] = W[p][4ks+t]
+        }
         cx += 4;
         if (cx >= RX) {
           cx -= RX;
@@ -371,41 +382,50 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, S.gB[ks][nt][d][lane]);
-      }
-      // stage 2: C[g][2t+i] = T_d[p0+g][z = 8nt + 2t + i]
-      double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+          for (int d = 0; d < 3; ++d) {
+            const double b = S.gB[ks][nt][d][lane];
 #pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt) {
-        const double2 wz = *reinterpret_cast<const double2*>(&sm.pz[pa][8 * nt + 2 * tq]);
-        e0 = fma(wz.x, acc[nt][0][0], fma(wz.y, acc[nt][0][1], e0));
-        e1 = fma(wz.x, acc[nt][1][0], fma(wz.y, acc[nt][1][1], e1));
-        e2 = fma(wz.x, acc[nt][2][0], fma(wz.y, acc[nt][2][1], e2));
+            for (int mt = 0; mt < C::MT; ++mt) dmma(acc[mt][nt][d], a[mt], b);
+          }
       }
 #pragma unroll
-      for (int o = 1; o <= 2; o <<= 1) {
-        e0 += __shfl_xor_sync(0xffffffffu, e0, o);
-        e1 += __shfl_xor_sync(0xffffffffu, e1, o);
-        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-      }
-      if (tq == 0 && pa < cnt) {
-        const int64_t j = base + pa;
-        if (Eout) {
-          const int64_t k = id[j];
-          Eout[k] = e0;
-          Eout[stride + k] = e1;
-          Eout[2 * stride + k] = e2;
+      for (int mt = 0; mt < C::MT; ++mt) {
+        const int pa = p0 + 8 * mt + gr;
+        if (p0 + 8 * mt >= pad) break;
+        // stage 2: C[g][2t+i] = T_d[p][z = 8nt + 2t + i]
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) {
+          const double2 wz = *reinterpret_cast<const double2*>(&sm.pz[pa][8 * nt + 2 * tq]);
+          e0 = fma(wz.x, acc[mt][nt][0][0], fma(wz.y, acc[mt][nt][0][1], e0));
+          e1 = fma(wz.x, acc[mt][nt][1][0], fma(wz.y, acc[mt][nt][1][1], e1));
+          e2 = fma(wz.x, acc[mt][nt][2][0], fma(wz.y, acc[mt][nt][2][1], e2));
         }
-        if (P.kicks > 0 || P.drift) {
-          double x0 = S.xv[buf][0][pa], x1 = S.xv[buf][1][pa], x2 = S.xv[buf][2][pa];
-          double v0 = S.xv[buf][3][pa], v1 = S.xv[buf][4][pa], v2 = S.xv[buf][5][pa];
-          push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
-          x[j] = x0;
-          x[stride + j] = x1;
-          x[2 * stride + j] = x2;
-          v[j] = v0;
-          v[stride + j] = v1;
-          v[2 * stride + j] = v2;
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+          e0 += __shfl_xor_sync(0xffffffffu, e0, o);
+          e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+          e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        }
+        if (tq == 0 && pa < cnt) {
+          const int64_t j = base + pa;
+          if (Eout) {
+            const int64_t k = id[j];
+            Eout[k] = e0;
+            Eout[stride + k] = e1;
+            Eout[2 * stride + k] = e2;
+          }
+          if (P.kicks > 0 || P.drift) {
+            double x0 = S.xv[buf][0][pa], x1 = S.xv[buf][1][pa], x2 = S.xv[buf][2][pa];
+            double v0 = S.xv[buf][3][pa], v1 = S.xv[buf][4][pa], v2 = S.xv[buf][5][pa];
+            push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
+            x[j] = x0;
+            x[stride + j] = x1;
+            x[2 * stride + j] = x2;
+            v[j] = v0;
+            v[stride + j] = v1;
+            v[2 * stride + j] = v2;
+          }
         }
       }
     }
