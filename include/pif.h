@@ -56,7 +56,8 @@ typedef enum {
   PIF_OK = 0,
   PIF_ERR_ARG = 1,     /* null pointer, size mismatch, N odd or < 2, tol out of [1e-15,1e-1), dt <= 0, L <= 0 */
   PIF_ERR_CONFIG = 2,  /* inconsistent configuration (see each call) */
-  PIF_ERR_NUMERIC = 3, /* non-finite state detected */
+  PIF_ERR_NUMERIC = 3, /* non-finite value detected: checked by pif_set_state (input),
+                          pif_get_state, pif_field_energy and each parareal correction */
   PIF_ERR_CUDA = 4,    /* CUDA runtime / cuFFT error (message has the code) */
   PIF_ERR_NCCL = 5,    /* NCCL error */
   PIF_ERR_OOM = 6,     /* workspace too small */
@@ -126,7 +127,8 @@ pif_status pif_workspace_size(pif_ctx ctx, size_t* bytes);
 pif_status pif_set_workspace(pif_ctx ctx, void* dptr, size_t bytes);
 
 /* Copy the local state in ([3][n_local] SoA each).  on_device = 1: CUDA
-   pointers; 0: host pointers (pinned or pageable).  Resets the time level. */
+   pointers; 0: host pointers (pinned or pageable).  Resets the time level.
+   Synchronises; PIF_ERR_NUMERIC (and no state) if any value is non-finite. */
 pif_status pif_set_state(pif_ctx ctx, const double* x, const double* v, int64_t n_local,
                          int on_device);
 /* Copy the local state out at an integer time level, in the ORIGINAL particle

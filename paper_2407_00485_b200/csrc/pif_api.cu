@@ -297,7 +297,9 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     // (RX RY) % 32 == 0).  w = 13 (eps = 1e-12): interpolation tiles 16x14x16
     // over 4x2x4-cell sub-bricks, spreading tiles 16^3 over 4^3-cell bricks.
     int RI[3], m[3] = {1, 1, 1};
-    if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
+    if (w == 5) { RI[0] = RI[1] = 6; RI[2] = 8; m[0] = m[1] = 2; }      // eps 1e-4: spread 8^3
+    else if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
+    else if (w == 8) { RI[0] = RI[1] = 10; RI[2] = 8; m[0] = m[1] = 3; }  // eps 1e-7: spread 16x16x8
     else if (w <= 9) { RI[0] = RI[1] = RI[2] = 12; }
 #ifndef PIF_W13_TILE
 #define PIF_W13_TILE 1
@@ -525,6 +527,18 @@ pif_status step_internal(pif_ctx c, int which, int64_t nsteps) {
   return PIF_OK;
 }
 
+// PIF_ERR_NUMERIC check: any non-finite value in a[0..count) (synchronises).
+pif_status check_finite(pif_ctx c, const double* a, int64_t count, const char* what) {
+  CU(cudaMemsetAsync(c->flag, 0, sizeof(int), c->st));
+  CU(launch_check_finite(a, count, c->flag, c->st));
+  CU(cudaMemcpyAsync(&c->host_red[12], c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  int bad = 0;
+  memcpy(&bad, &c->host_red[12], sizeof(int));
+  if (bad) return fail(PIF_ERR_NUMERIC, std::string("non-finite values in ") + what);
+  return PIF_OK;
+}
+
 // Canonical-order state buffer: [x(3n) | v(3n) | flag(1)] doubles.
 struct State {
   double* p = nullptr;
@@ -737,7 +751,9 @@ pif_status pif_set_state(pif_ctx c, const double* x, const double* v, int64_t n_
   CU(cudaMemcpyAsync(c->xA, x, b, k, c->st));
   CU(cudaMemcpyAsync(c->vA, v, b, k, c->st));
   CU(launch_iota(c->idA, n_local, c->st));
-  if (!on_device) CU(cudaStreamSynchronize(c->st));
+  c->has_state = false;
+  TRY(check_finite(c, c->xA, 3 * n_local, "the input positions"));
+  TRY(check_finite(c, c->vA, 3 * n_local, "the input velocities"));
   c->has_state = true;
   c->pending = false;
   c->box_fresh = false;
@@ -751,6 +767,8 @@ pif_status pif_get_state(pif_ctx c, double* x, double* v, int64_t n_local, int o
   TRY(materialize(c));
   const int64_t n = c->nloc;
   CU(launch_scatter_by_id(c->xA, c->vA, c->idA, n, n, c->xB, c->vB, c->st));
+  TRY(check_finite(c, c->xB, 3 * n, "the positions"));
+  TRY(check_finite(c, c->vB, 3 * n, "the velocities"));
   cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   CU(cudaMemcpyAsync(x, c->xB, 3 * n * sizeof(double), k, c->st));
   CU(cudaMemcpyAsync(v, c->vB, 3 * n * sizeof(double), k, c->st));
@@ -795,6 +813,8 @@ pif_status pif_field_energy(pif_ctx c, double W[3], double* kinetic, double mome
   }
   *kinetic = 0.5 * c->m * r[4];
   for (int d = 0; d < 3; ++d) momentum[d] = c->m * r[5 + d];
+  for (int q = 0; q < 8; ++q)
+    if (!std::isfinite(r[q])) return fail(PIF_ERR_NUMERIC, "non-finite field energy / moments");
   return PIF_OK;
 }
 
@@ -872,6 +892,8 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
     const double* r = c->host_red;
     ex = r[1] > 0 ? std::sqrt(r[0] / r[1]) : std::sqrt(r[0]);
     ev = r[3] > 0 ? std::sqrt(r[2] / r[3]) : std::sqrt(r[2]);
+    if (!std::isfinite(ex) || !std::isfinite(ev))
+      return fail(PIF_ERR_NUMERIC, "non-finite parareal state (stopping norms)");
     return PIF_OK;
   };
 

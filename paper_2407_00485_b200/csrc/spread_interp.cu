@@ -465,6 +465,7 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
     return spread_launch<A, B, Cz>(nbr, x, stride, s, s_uniform, offsets, g, hc, grid, st);
   PIF_SPREAD(8, 8, 8)
   PIF_SPREAD(12, 12, 12)
+  PIF_SPREAD(16, 16, 8)
   PIF_SPREAD(16, 16, 16)
 #undef PIF_SPREAD
   return cudaErrorInvalidValue;
@@ -495,7 +496,9 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
 #define PIF_INTERP(A, B, Cz)                                                                   \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
+  PIF_INTERP(6, 6, 8)
   PIF_INTERP(8, 8, 8)
+  PIF_INTERP(10, 10, 8)
   PIF_INTERP(12, 12, 12)
   PIF_INTERP(14, 14, 16)
   PIF_INTERP(16, 14, 16)

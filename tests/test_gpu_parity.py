@@ -371,3 +371,34 @@ def test_two_stream_growth_rate_C3():
     root = _dispersion_root(N, phys.L, 0.5, 0.3j, sigma=0.1, vb=math.pi / 2)
     assert abs(root.imag - 0.31615) < 2e-3, root
     assert abs(slope - root.imag) < 0.10 * root.imag, (slope, root)
+
+
+def test_error_paths():
+    """pif_status behaviour on the GPU: non-finite input -> PIF_ERR_NUMERIC (state
+    rejected); step before set_state -> PIF_ERR_STATE; n_local mismatch -> ARG;
+    parareal interval not a multiple of dt -> CONFIG."""
+    phys = landau_physics()
+    x0, v0 = landau_state(1000, 15)
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=1e-7), P.propagator("pic", 8, 0.1), n=1000)
+    with pytest.raises(P.PifError) as e:
+        sim.step(1)
+    assert e.value.status == 7
+    bad = v0.copy()
+    bad[1, 17] = np.nan
+    with pytest.raises(P.PifError) as e:
+        sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(bad).cuda())
+    assert e.value.status == 3
+    with pytest.raises(P.PifError) as e:
+        sim.step(1)  # the rejected state was not installed
+    assert e.value.status == 7
+    with pytest.raises(P.PifError) as e:
+        P.pif_set_state(sim.ctx, torch.from_numpy(x0[:, :999].copy()).cuda(),
+                        torch.from_numpy(v0[:, :999].copy()).cuda())
+    assert e.value.status == 1
+    sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
+    with pytest.raises(P.PifError) as e:
+        sim.parareal(0.0, 0.33, 2, 2, 1e-6)
+    assert e.value.status == 2
+    sim.step(2)
+    x, v = sim.get_state()
+    assert torch.isfinite(x).all() and torch.isfinite(v).all()
