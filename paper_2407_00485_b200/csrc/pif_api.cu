@@ -296,10 +296,14 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     // Tile shapes (DMMA needs RZ % 8 == 0 for spreading and
     // (RX RY) % 32 == 0).  w = 13 (eps = 1e-12): interpolation tiles 16x14x16
     // over 4x2x4-cell sub-bricks, spreading tiles 16^3 over 4^3-cell bricks.
+    // Small tiles waste fewer FMAs on padding but carry fewer particles per CTA;
+    // below ~12 (w = 8) / ~8 (w = 5) particles per upsampled cell the per-CTA
+    // overheads win, so the larger tiles are kept there (measured).
+    const double ppc = (double)c->nloc / ((double)n * n * n);
     int RI[3], m[3] = {1, 1, 1};
-    if (w == 5) { RI[0] = RI[1] = 6; RI[2] = 8; m[0] = m[1] = 2; }      // eps 1e-4: spread 8^3
+    if (w == 5 && ppc >= 8.0) { RI[0] = RI[1] = 6; RI[2] = 8; m[0] = m[1] = 2; }      // spread 8^3
     else if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
-    else if (w == 8) { RI[0] = RI[1] = 10; RI[2] = 8; m[0] = m[1] = 3; }  // eps 1e-7: spread 16x16x8
+    else if (w == 8 && ppc >= 12.0) { RI[0] = RI[1] = 10; RI[2] = 8; m[0] = m[1] = 3; }  // spread 16x16x8
     else if (w <= 9) { RI[0] = RI[1] = RI[2] = 12; }
 #ifndef PIF_W13_TILE
 #define PIF_W13_TILE 1

@@ -58,6 +58,22 @@ def test_type2_vs_nudft_C1(tol):
     assert rel_l2(got, ref) <= 10 * tol
 
 
+@pytest.mark.parametrize("tol", [1e-7, 1e-4])
+def test_type1_type2_dense_tiles(tol):
+    """>= 12 particles per upsampled cell (16^3 grid) selects the small dense tiles
+    (interp 10x10x8 / 6x6x8); ragged count."""
+    phys = landau_physics()
+    npart = 16 * 16 ** 3 + 7
+    x, _ = landau_state(npart, 5)
+    rng = np.random.default_rng(5)
+    s = rng.standard_normal(npart)
+    c = rng.standard_normal((8, 8, 8)) + 1j * rng.standard_normal((8, 8, 8))
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=tol), n=npart)
+    assert sim.plan_info(0)[2] == 16
+    assert rel_l2(P.pif_debug_type1(sim.ctx, 0, x, s, 8), O.nudft_type1(x, s, 8, phys.L)) <= 10 * tol
+    assert rel_l2(P.pif_debug_type2(sim.ctx, 0, c, x), O.nudft_type2(c, x, 8, phys.L)) <= 10 * tol
+
+
 @pytest.mark.parametrize("N,npart", [(2, 1), (6, 37), (16, 5000), (32, 20000)])
 def test_type1_type2_ragged_and_edge_sizes(N, npart):
     """Tiny / ragged particle counts, N = 2 (only Nyquist and k=0), larger N."""
