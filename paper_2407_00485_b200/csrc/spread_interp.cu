@@ -32,11 +32,7 @@ namespace pif {
 #ifndef PIF_CHUNK
 #define PIF_CHUNK 128
 #endif
-#ifndef PIF_ICHUNK
-#define PIF_ICHUNK 64
-#endif
 constexpr int kChunk = PIF_CHUNK;    // spread: particles staged per shared-memory round
-constexpr int kIChunk = PIF_ICHUNK;  // interp: smaller, so two CTAs fit per SM
 
 #ifdef PIF_DMMA_NONVOLATILE
 #define PIF_DMMA_ASM asm
@@ -58,6 +54,43 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// 8-byte cp.async that writes zeros (reads nothing) when !valid.
+__device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0)
+               : "memory");
+}
+
+// mbarrier (shared memory, CTA scope).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// arrive on b once every cp.async this thread issued so far has landed
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// Wait for completion of the phase with the given parity.  Bounded: a protocol
+// error traps (kernel error) after ~10 s instead of hanging the device.
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
+  unsigned done = 0;
+  long long t0 = 0;
+  for (int spin = 0;; ++spin) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin == 0) t0 = clock64();
+    else if (clock64() - t0 > 20000000000LL) __trap();
+  }
+}
 
 // psi row strides (doubles): S == 4 or 12 (mod 16) so that the 4 particle rows
 // read by one half-warp fragment load (4 consecutive doubles each) fall in
@@ -256,38 +289,78 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
 // "K = columns" formulation: every warp owns whole m-tiles of 8 particles and
 // contracts over all tile columns,
 //   T_d[p][z] = sum_c W[p][c] g_d[c][z],   W[p][c] = psi_x[p][cx] psi_y[p][cy]
-// (M = particles, K = columns, N = z), with the g tile staged once per CTA in
-// shared memory in B-fragment order (one conflict-free LDS.64 per DMMA) and A
-// formed by one DMUL per fragment element.  Stage 2, E_d[p] = sum_z psi_z[p][z]
-// T_d[p][z], is 16 values per particle inside the warp; the warp pushes its own
-// particles, so the m-tile loop has no block barrier.  DMMA and DFMA share the
-// FP64 pipe on B200 (profiles/r1_dmma_mix.log), so the vector work is kept to
-// ~3 % of the MMA FMAs.
+// (M = particles, K = columns, N = z), with the g tile in shared memory in
+// B-fragment order (one conflict-free LDS.64 per DMMA) and A formed by one DMUL
+// per fragment element.  Stage 2, E_d[p] = sum_z psi_z[p][z] T_d[p][z], is 16
+// values per particle inside the warp, and the warp pushes its own particles.
+//
+// Persistent and warp-specialised: one producer warp streams the g tiles of the
+// CTA's items (blockIdx.x, + gridDim.x, ...) into a double buffer with cp.async,
+// completion signalled on mbarriers full[b]; NW consumer warps walk the CTA's
+// concatenated m-tile sequence round-robin, each with its own x, v cp.async
+// double buffer and psi rows (24 lanes = 8 particles x 3 dimensions, Horner
+// groups warp-uniform), and release a tile buffer (empty[b]) once past its item.
+// No CTA barrier after setup: a warp done with item k starts on item k+1 while
+// others finish k, and the tile of item k+1 loads during item k.  DMMA and DFMA
+// share the FP64 pipe on B200 (profiles/r1_dmma_mix.log): the vector work is
+// ~7 % of the MMA FMAs.
 template <int RX, int RY, int RZ>
 struct InterpCfg {
   static constexpr int NC = RX * RY;       // tile columns (K)
   static constexpr int KS = NC / 4;        // k steps
   static constexpr int NT = (RZ + 7) / 8;  // z n-tiles of 8 (psi_z rows zero-padded)
-#ifndef PIF_INW
-#define PIF_INW 8
-#endif
-#ifndef PIF_IMT
-#define PIF_IMT 1
-#endif
-  static constexpr int MT = PIF_IMT;  // m-tiles per warp pass (B-fragment reuse)
-  static constexpr int NW = PIF_INW;       // warps (m-tiles processed round-robin)
+  static constexpr int ZP = NT * 8;        // padded z extent
+  // warp-private psi rows: px[8][SX] at 0, py[8][SY] at OY, pz[8][SZ] at OZ.
+  // Row strides = 4 or 12 (mod 16) doubles keep the A-fragment reads
+  // conflict-free; the 1 / 2 double offsets of py / pz put the 24 staging lanes'
+  // row writes (particle p of x, y, z) in different banks.
+  static constexpr int SX = RowStride<RX>::v, SY = RowStride<RY>::v, SZ = RowStride<ZP>::v;
+  static constexpr int OY = 8 * SX + 1, OZ = OY + 8 * SY + 1;
+  static constexpr int WP = OZ + 8 * SZ;   // psi doubles per warp (even: 16-byte aligned)
+  static constexpr int GB = KS * NT * 3 * 32;  // doubles per g-tile buffer
+  // consumer warps: as many as fit (<= 16) next to the double-buffered tile in
+  // the 227 KB of dynamic shared memory a CTA may use
+  static constexpr int BUDGET = (232448 - 64) / 8 - 2 * GB;
+  static constexpr int NWFIT = BUDGET / (WP + 96);
+  static constexpr int NW = NWFIT < 16 ? NWFIT : 16;
   static_assert(NC % 4 == 0, "tile columns must be a multiple of 4");
+  static_assert(OZ % 2 == 0 && WP % 2 == 0, "pz rows are read as double2");
+  static_assert(NW >= 4, "tile too large for the persistent interpolation kernel");
 };
 
 template <int RX, int RY, int RZ>
 struct InterpSmem {
-  double gB[InterpCfg<RX, RY, RZ>::KS][InterpCfg<RX, RY, RZ>::NT][3][32];  // B fragments
-  Psi<RX, RY, RZ, kIChunk> psi;
-  double xv[2][6][kIChunk];  // x, v of the current / next chunk (cp.async double buffer)
+  using C = InterpCfg<RX, RY, RZ>;
+  double gB[2][C::KS][C::NT][3][32];  // B fragments, double-buffered over items
+  double psi[C::NW][C::WP];           // per-warp psi rows
+  double xv[C::NW][2][6][8];          // per-warp x, v double buffer (cp.async)
+  unsigned long long full[2], empty[2];
 };
 
+// An interpolation item of this CTA (the k-th: item blockIdx.x + k gridDim.x)
+// and its m-tiles [base, base + m) in the CTA's concatenated sequence.
+struct ItemCursor {
+  int k, base, m;
+  int64_t start, end;
+  int T0[3];
+};
+
+__device__ __forceinline__ void cursor_load(ItemCursor& it, const Brick& g, const Sched& Sc) {
+  const int4 e = Sc.iitems[blockIdx.x + (int64_t)it.k * gridDim.x];
+  it.start = e.y;
+  it.end = e.z;
+  it.m = (int)((e.z - e.y + 7) >> 3);
+  const int M = g.m[0] * g.m[1] * g.m[2];
+  const int brick = e.x / M, sk = e.x % M;
+  const int bz = brick % g.NB[2], by = (brick / g.NB[2]) % g.NB[1], bx = brick / (g.NB[2] * g.NB[1]);
+  const int sz = sk % g.m[2], sy = (sk / g.m[2]) % g.m[1], sx = sk / (g.m[2] * g.m[1]);
+  it.T0[0] = bx * g.sb[0] - g.hw + sx * g.ib[0];
+  it.T0[1] = by * g.sb[1] - g.hw + sy * g.ib[1];
+  it.T0[2] = bz * g.sb[2] - g.hw + sz * g.ib[2];
+}
+
 template <int RX, int RY, int RZ>
-__global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
+__global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
     k_interp_push(const double* __restrict__ grid3, double* __restrict__ x,
                   double* __restrict__ v, int64_t stride, const int* __restrict__ id,
                   double* __restrict__ Eout, const Sched Sc, Brick g,
@@ -295,142 +368,221 @@ __global__ void __launch_bounds__(32 * InterpCfg<RX, RY, RZ>::NW, 2)
   using C = InterpCfg<RX, RY, RZ>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   InterpSmem<RX, RY, RZ>& S = *reinterpret_cast<InterpSmem<RX, RY, RZ>*>(smem_raw);
-  Psi<RX, RY, RZ, kIChunk>& sm = S.psi;
-  int T0[3];
-  int64_t start, end;
-  if (!tile_of(g, Sc, true, T0, start, end)) return;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int gr = lane >> 2, tq = lane & 3;
+  const int total = Sc.ioff[Sc.nkeys];
+  const int G = gridDim.x;
+  const int nitems = (int)blockIdx.x < total ? (total - (int)blockIdx.x + G - 1) / G : 0;
+  if (nitems == 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n = g.n;
   const int64_t n3 = (int64_t)n * n * n;
-
-  // x, v of chunk i+1 stream into S.xv[(i+1)&1] with cp.async during chunk i
-  auto prefetch = [&](int buf, int64_t b, int c) {
-    for (int r = tid; r < c; r += blockDim.x) {
-      const int64_t j = b + r;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) cp_async8(&S.xv[buf][q][r], x + q * stride + j);
-      if (v)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) cp_async8(&S.xv[buf][3 + q][r], v + q * stride + j);
-    }
-    cp_async_commit();
-  };
-  prefetch(0, start, (int)min((int64_t)kIChunk, end - start));
-
-  // g tile -> B fragments: gB[ks][nt][d][l] = g_d[c = 4 ks + (l & 3)][z = 8 nt + (l >> 2)]
-  // (consecutive threads read consecutive z of one column: coalesced)
-  {
-    // g tile -> smem B fragments with cp.async (overlaps the first chunk's
-    // staging); one (component, column) pair per ZP lanes, one z per lane
-    constexpr int ZP = C::NT * 8;           // padded z extent (8 or 16)
-    constexpr int PER = 32 / ZP;            // (d, c) pairs per warp step
-    const int zl = lane % ZP, sub = lane / ZP;
-    int gz = T0[2] + zl;
-    gz = gz < 0 ? gz + n : (gz >= n ? gz - n : gz);
-    for (int dc = wid * PER + sub; dc < 3 * C::NC; dc += C::NW * PER) {
-      const int d = dc / C::NC, c = dc - d * C::NC;
-      const int cy = c / RX, cx = c - cy * RX;
-      int gx = T0[0] + cx, gy = T0[1] + cy;
-      gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
-      gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
-      double* dst = &S.gB[c >> 2][zl >> 3][d][((zl & 7) << 2) | (c & 3)];
-      if (zl < RZ) cp_async8(dst, grid3 + d * n3 + ((int64_t)gx * n + gy) * n + gz);
-      else *dst = 0.0;
-    }
-    cp_async_commit();
+  if (threadIdx.x == 0) {
+    mbar_init(&S.full[0], 32);
+    mbar_init(&S.full[1], 32);
+    mbar_init(&S.empty[0], C::NW);
+    mbar_init(&S.empty[1], C::NW);
   }
+  __syncthreads();
 
-  int buf = 0;
-  for (int64_t base = start; base < end; base += kIChunk, buf ^= 1) {
-    const int cnt = (int)min((int64_t)kIChunk, end - base);
-    const int pad = (cnt + 7) & ~7;
-    // chunk 0: x/v (group 0) may land before the g tile (group 1)
-    if (base == start) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else cp_async_wait_all();
-    __syncthreads();  // every thread's cp.async data for this chunk is visible
-    for (int q = tid; q < cnt; q += blockDim.x) {
-      const double xr[3] = {S.xv[buf][0][q], S.xv[buf][1][q], S.xv[buf][2][q]};
-      stage_position(sm, q, xr, g, T0);
-    }
-    if (base == start) cp_async_wait_all();  // g tile landed (published by stage_psi's barriers)
-    stage_psi<true>(sm, cnt, pad, g, T0, hc);
-    if (base + kIChunk < end) prefetch(buf ^ 1, base + kIChunk, (int)min((int64_t)kIChunk, end - base - kIChunk));
-    // each warp takes C::MT m-tiles of 8 particles at once: every smem B fragment feeds C::MT DMMAs
-    for (int p0 = 8 * C::MT * wid; p0 < pad; p0 += 8 * C::MT * C::NW) {
-      double acc[C::MT][C::NT][3][2];
+  if (wid == C::NW) {
+    // ---- producer: g tile of item k -> gB[k & 1], stored lane-permuted:
+    // B[t][g] = g_d[c = 4 ks + t][z = 8 nt + g] at gB[.][ks][nt][d][e],
+    // e = 16 (g >> 2) + 4 t + (g & 3): each half-warp of a fragment read (g = 0..3
+    // or 4..7) hits 16 distinct 8-byte bank slots, and the stores come in
+    // 128-byte blocks of 4 columns x 4 z (lane = (h = g >> 2, t, zq = g & 3)).
+    const int h = (lane >> 4) & 1, t = (lane >> 2) & 3, zq = lane & 3;
+    const int eoff = (h << 4) | (t << 2) | zq;
+    ItemCursor it;
+    for (it.k = 0; it.k < nitems; ++it.k) {
+      const int b = it.k & 1;
+      if (it.k >= 2) mbar_wait(&S.empty[b], ((it.k >> 1) - 1) & 1);
+      cursor_load(it, g, Sc);
+      int gz[C::NT];
+      bool zin[C::NT];
 #pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt)
+      for (int nt = 0; nt < C::NT; ++nt) {
+        const int zl = 8 * nt + 4 * h + zq;
+        const int z = it.T0[2] + zl;
+        gz[nt] = z < 0 ? z + n : (z >= n ? z - n : z);
+        zin[nt] = zl < RZ;
+      }
+      int cx = t % RX, cy = t / RX;
+      for (int ks = 0; ks < C::KS; ++ks) {
+        int gx = it.T0[0] + cx, gy = it.T0[1] + cy;
+        gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
+        gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
+        const double* src = grid3 + ((int64_t)gx * n + gy) * n;
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) acc[mt][nt][d][0] = acc[mt][nt][d][1] = 0.0;
-      int cx = tq % RX, cy = tq / RX;  // column c = 4 ks + tq, advanced incrementally
-#pragma unroll 2
-      for (int ks = 0; ks < C::KS; ++ks) {
-        double a[C::MT];
-#pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) {
-          const int pa = min(p0 + 8 * mt + gr, kIChunk - 1);  // rows >= pad hold zero psi
-          a[mt] = sm.px[pa][cx] * sm.py[pa][cy];  // A[g][t] = W[p][4ks+t]
-        }
+          for (int d = 0; d < 3; ++d)
+            cp_async8_zfill(&S.gB[b][ks][nt][d][eoff], src + d * n3 + gz[nt], zin[nt]);
         cx += 4;
         if (cx >= RX) {
           cx -= RX;
           cy += 1;
         }
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double b = S.gB[ks][nt][d][lane];
-#pragma unroll
-            for (int mt = 0; mt < C::MT; ++mt) dmma(acc[mt][nt][d], a[mt], b);
-          }
       }
-#pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt) {
-        const int pa = p0 + 8 * mt + gr;
-        if (p0 + 8 * mt >= pad) break;
-        // stage 2: C[g][2t+i] = T_d[p][z = 8nt + 2t + i]
-        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt) {
-          const double2 wz = *reinterpret_cast<const double2*>(&sm.pz[pa][8 * nt + 2 * tq]);
-          e0 = fma(wz.x, acc[mt][nt][0][0], fma(wz.y, acc[mt][nt][0][1], e0));
-          e1 = fma(wz.x, acc[mt][nt][1][0], fma(wz.y, acc[mt][nt][1][1], e1));
-          e2 = fma(wz.x, acc[mt][nt][2][0], fma(wz.y, acc[mt][nt][2][1], e2));
-        }
-#pragma unroll
-        for (int o = 1; o <= 2; o <<= 1) {
-          e0 += __shfl_xor_sync(0xffffffffu, e0, o);
-          e1 += __shfl_xor_sync(0xffffffffu, e1, o);
-          e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-        }
-        if (tq == 0 && pa < cnt) {
-          const int64_t j = base + pa;
-          if (Eout) {
-            const int64_t k = id[j];
-            Eout[k] = e0;
-            Eout[stride + k] = e1;
-            Eout[2 * stride + k] = e2;
-          }
-          if (P.kicks > 0 || P.drift) {
-            double x0 = S.xv[buf][0][pa], x1 = S.xv[buf][1][pa], x2 = S.xv[buf][2][pa];
-            double v0 = S.xv[buf][3][pa], v1 = S.xv[buf][4][pa], v2 = S.xv[buf][5][pa];
-            push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
-            x[j] = x0;
-            x[stride + j] = x1;
-            x[2 * stride + j] = x2;
-            v[j] = v0;
-            v[stride + j] = v1;
-            v[2 * stride + j] = v2;
-          }
+      cp_async_mbar_arrive(&S.full[b]);
+    }
+    cp_async_wait_all();
+    return;
+  }
+
+  // ---- consumers
+  const int gr = lane >> 2, tq = lane & 3;
+  const int lperm = ((gr >> 2) << 4) | (tq << 2) | (gr & 3);  // this lane's B-fragment entry
+  double* const wpsi = S.psi[wid];
+  double (*const xv)[6][8] = S.xv[wid];
+  const double two_over_w = 2.0 / g.w;
+  const double flo = g.odd ? -0.5 : 0.0;
+
+  // cursor c: the item of the m-tile being computed; passing an item releases
+  // its tile buffer (after its tile is known to have landed, so that this warp's
+  // arrivals on empty[b] stay in phase order).  Cursor pf: x, v prefetch.
+  ItemCursor c, pf;
+  c.k = pf.k = 0;
+  c.base = pf.base = 0;
+  cursor_load(c, g, Sc);
+  pf = c;
+  auto advance = [&](ItemCursor& it, int q, bool release) {
+    while (it.k < nitems && q >= it.base + it.m) {
+      if (release) {
+        mbar_wait(&S.full[it.k & 1], (it.k >> 1) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[it.k & 1]);
+      }
+      it.base += it.m;
+      if (++it.k < nitems) cursor_load(it, g, Sc);
+    }
+    return it.k < nitems;
+  };
+  // x, v of m-tile q -> xv[buf] (one cp.async group, possibly empty)
+  auto prefetch = [&](int buf, int q) {
+    if (advance(pf, q, false)) {
+      const int64_t b = pf.start + 8 * (int64_t)(q - pf.base);
+      const int cnt = (int)min((int64_t)8, pf.end - b);
+      for (int u = lane; u < 48; u += 32) {
+        const int comp = u >> 3, p = u & 7;
+        if (p < cnt) {
+          if (comp < 3) cp_async8(&xv[buf][comp][p], x + comp * stride + b + p);
+          else if (v) cp_async8(&xv[buf][comp][p], v + (comp - 3) * stride + b + p);
         }
       }
     }
-    __syncthreads();  // psi rows / S.xv[buf] are reused by the next chunks
+    cp_async_commit();
+  };
+  // psi rows of the current m-tile (cnt particles): lane = (particle p,
+  // dimension d) for lanes < 24; zero row, then the w window weights (edge
+  // nodes exactly, interior nodes by Horner groups of 4: warp-uniform constants)
+  auto stage = [&](int buf, int cnt) {
+    if (lane < 24) {
+      const int p = lane & 7, d = lane >> 3;
+      const int R = d == 0 ? RX : (d == 1 ? RY : C::ZP);
+      double* row = wpsi + (d == 0 ? p * C::SX : (d == 1 ? C::OY + p * C::SY : C::OZ + p * C::SZ));
+#pragma unroll
+      for (int u = 0; u < (RX > C::ZP ? RX : (RY > C::ZP ? RY : C::ZP)); ++u)
+        if (u < R) row[u] = 0.0;
+      if (p < cnt) {
+        const int w = g.w;
+        const int T0d = d == 0 ? c.T0[0] : (d == 1 ? c.T0[1] : c.T0[2]);
+        double xs = xv[buf][d][p] * g.scale;
+        const int a = anchor_of(xs, g);
+        const double f = xs - (double)a;
+        double* wrow = row + (a - g.hw - T0d);
+        wrow[0] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
+        wrow[w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+        const double sv = 2.0 * (f - flo) - 1.0;
+        const int ngroups = (w - 2 + 3) / 4;
+        for (int gg = 0; gg < ngroups; ++gg) {
+          const int k0 = 1 + 4 * gg;
+          double acc[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = hc.a[min(k0 + q, 15)][kHornerDeg];
+#pragma unroll
+          for (int j = kHornerDeg - 1; j >= 0; --j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(acc[q], sv, hc.a[min(k0 + q, 15)][j]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (k0 + q < w - 1) wrow[k0 + q] = acc[q];
+        }
+      }
+    }
+  };
+
+  int buf = 0;
+  prefetch(0, wid);
+  for (int q = wid; advance(c, q, true); q += C::NW, buf ^= 1) {
+    const int64_t b = c.start + 8 * (int64_t)(q - c.base);
+    const int cnt = (int)min((int64_t)8, c.end - b);
+    prefetch(buf ^ 1, q + C::NW);  // xv[buf ^ 1] was released by the previous m-tile
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    stage(buf, cnt);
+    const int tb = c.k & 1;
+    mbar_wait(&S.full[tb], (c.k >> 1) & 1);  // g tile of this item landed
+    __syncwarp();                            // psi rows visible to the warp
+    double acc[C::NT][3][2];
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) acc[nt][d][0] = acc[nt][d][1] = 0.0;
+    const double* pxr = wpsi + gr * C::SX;
+    const double* pyr = wpsi + C::OY + gr * C::SY;
+    const double* gBt = &S.gB[tb][0][0][0][0] + lperm;
+    int cx = tq % RX, cy = tq / RX;  // column c = 4 ks + tq, advanced incrementally
+#pragma unroll 2
+    for (int ks = 0; ks < C::KS; ++ks) {
+      const double a = pxr[cx] * pyr[cy];  // A[g][t] = W[p][4ks+t]
+      cx += 4;
+      if (cx >= RX) {
+        cx -= RX;
+        cy += 1;
+      }
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, gBt[((ks * C::NT + nt) * 3 + d) * 32]);
+    }
+    // stage 2: C[g][2t+i] = T_d[p][z = 8nt + 2t + i]
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    const double* pzr = wpsi + C::OZ + gr * C::SZ;
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) {
+      const double2 wz = *reinterpret_cast<const double2*>(pzr + 8 * nt + 2 * tq);
+      e0 = fma(wz.x, acc[nt][0][0], fma(wz.y, acc[nt][0][1], e0));
+      e1 = fma(wz.x, acc[nt][1][0], fma(wz.y, acc[nt][1][1], e1));
+      e2 = fma(wz.x, acc[nt][2][0], fma(wz.y, acc[nt][2][1], e2));
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      e0 += __shfl_xor_sync(0xffffffffu, e0, o);
+      e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+      e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    }
+    if (tq == 0 && gr < cnt) {
+      const int64_t j = b + gr;
+      if (Eout) {
+        const int64_t k = id[j];
+        Eout[k] = e0;
+        Eout[stride + k] = e1;
+        Eout[2 * stride + k] = e2;
+      }
+      if (P.kicks > 0 || P.drift) {
+        double x0 = xv[buf][0][gr], x1 = xv[buf][1][gr], x2 = xv[buf][2][gr];
+        double v0 = xv[buf][3][gr], v1 = xv[buf][4][gr], v2 = xv[buf][5][gr];
+        push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
+        x[j] = x0;
+        x[stride + j] = x1;
+        x[2 * stride + j] = x2;
+        v[j] = v0;
+        v[stride + j] = v1;
+        v[2 * stride + j] = v2;
+      }
+    }
+    __syncwarp();  // psi rows and xv[buf] are rewritten for the next m-tile
   }
+  cp_async_wait_all();
 }
 
 template <int A, int B, int Cz>
@@ -476,16 +628,24 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
                                  int64_t stride, const int* id, double* Eout, const Sched& offsets,
                                  const Brick& g, const Horner& hc, const PushArgs& P,
                                  cudaStream_t st) {
-  const int T = 32 * InterpCfg<A, B, Cz>::NW;
+  const int T = 32 * (InterpCfg<A, B, Cz>::NW + 1);
   const size_t smem = sizeof(InterpSmem<A, B, Cz>);
-  static bool attr = false;
-  if (!attr) {
+  static int ctas = 0;  // persistent grid: SMs x resident CTAs per SM
+  if (!ctas) {
     cudaError_t e = cudaFuncSetAttribute(k_interp_push<A, B, Cz>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0, per = 0;
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push<A, B, Cz>, T, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (per < 1) return cudaErrorInvalidConfiguration;
+    ctas = sms * per;
   }
-  k_interp_push<A, B, Cz><<<nsub, T, smem, st>>>(grid3, x, v, stride, id, Eout, offsets, g, hc, P);
+  const unsigned grid = nsub < (unsigned)ctas ? nsub : (unsigned)ctas;
+  if (grid == 0) return cudaSuccess;
+  k_interp_push<A, B, Cz><<<grid, T, smem, st>>>(grid3, x, v, stride, id, Eout, offsets, g, hc, P);
   return cudaGetLastError();
 }
 
