@@ -9,14 +9,14 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 
-constexpr int KS = 49, NT = 2, NW = 8, SX = 20;
+constexpr int KS = 49, NT = 2, NW = 16, SX = 20;
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
 template <int V>
-__global__ void __launch_bounds__(256, 2) feed(double* out, int reps) {
+__global__ void __launch_bounds__(512, 1) feed(double* out, int reps) {
   extern __shared__ double sm[];
   double* gB = sm;                         // [KS][NT][3][32]
   double* psi = sm + KS * NT * 3 * 32;     // [NW][2][8][SX] px / py rows
@@ -74,26 +74,26 @@ __global__ void __launch_bounds__(256, 2) feed(double* out, int reps) {
 }
 
 template <int V>
-void run(const char* name, int sms) {
+void run(const char* name, int sms, int warps = 8, int per_sm = 2) {
   const size_t smem = (KS * NT * 3 * 32 + NW * 2 * 8 * SX * 2) * sizeof(double);
   cudaFuncSetAttribute(feed<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   double* d;
   cudaMalloc(&d, 4096);
-  const int reps = 400, blocks = 2 * sms;
-  feed<V><<<blocks, 256, smem>>>(d, 2);
+  const int reps = 400, blocks = per_sm * sms;
+  feed<V><<<blocks, 32 * warps, smem>>>(d, 2);
   cudaDeviceSynchronize();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  feed<V><<<blocks, 256, smem>>>(d, reps);
+  feed<V><<<blocks, 32 * warps, smem>>>(d, reps);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   const int MT = V == 2 ? 2 : 1;
-  const double fl = 2.0 * 256 * KS * NT * 3 * MT * (double)reps * 8 * blocks;
-  printf("%-34s %.2f TFLOP/s (%s, smem %zu B)\n", name, fl / ms / 1e9,
+  const double fl = 2.0 * 256 * KS * NT * 3 * MT * (double)reps * warps * blocks;
+  printf("%-34s %2d warps x %d CTA/SM: %.2f TFLOP/s (%s, smem %zu B)\n", name, warps, per_sm, fl / ms / 1e9,
          cudaGetErrorString(cudaGetLastError()), smem);
   cudaFree(d);
 }
@@ -101,10 +101,12 @@ void run(const char* name, int sms) {
 int main() {
   cudaDeviceProp p;
   cudaGetDeviceProperties(&p, 0);
-  run<0>("V0 B in registers", p.multiProcessorCount);
-  run<1>("V1 LDS.64 per DMMA (interp)", p.multiProcessorCount);
-  run<2>("V2 2 m-tiles per B LDS.64", p.multiProcessorCount);
-  run<3>("V3 LDS.128 per 2 DMMA", p.multiProcessorCount);
-  run<1>("V1 again", p.multiProcessorCount);
+  const int sms = p.multiProcessorCount;
+  for (int w : {4, 8, 16}) {
+    run<0>("V0 B in registers", sms, w, 1);
+    run<1>("V1 LDS.64 per DMMA (interp)", sms, w, 1);
+    run<2>("V2 2 m-tiles per B LDS.64", sms, w, 1);
+    run<3>("V3 LDS.128 per 2 DMMA", sms, w, 1);
+  }
   return 0;
 }
