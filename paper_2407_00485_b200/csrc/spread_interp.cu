@@ -29,6 +29,9 @@
 
 namespace pif {
 
+#ifndef PIF_SPREAD_MINB
+#define PIF_SPREAD_MINB 3  // 3 CTAs/SM (shared memory allows 3 for the 16^3 tile)
+#endif
 #ifndef PIF_CHUNK
 #define PIF_CHUNK 128
 #endif
@@ -149,58 +152,61 @@ __device__ __forceinline__ void stage_position(Psi<RX, RY, RZ, CH>& sm, int tid,
   }
 }
 
+// Interior nodes 1 .. 4 NG of one psi row by Horner, all 4 NG chains in one
+// pass (14 dependent steps instead of 14 NG: the FP64 pipe is shared with the
+// other warps' DMMAs, so each dependent step waits behind them).
+template <int NG>
+__device__ __forceinline__ void horner_row(double* wrow, double f, double sv, const Horner& hc,
+                                           const Brick& g, double two_over_w) {
+  const int w = g.w;
+  // edge nodes exactly (sqrt singularity at |t| = w/2), independent of the chains below
+  wrow[0] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
+  wrow[w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+  double acc[4 * NG + 1];  // (+1: NG may be 0)
+#pragma unroll
+  for (int q = 0; q < 4 * NG; ++q) acc[q] = hc.a[min(1 + q, 15)][kHornerDeg];
+#pragma unroll
+  for (int j = kHornerDeg - 1; j >= 0; --j)
+#pragma unroll
+    for (int q = 0; q < 4 * NG; ++q) acc[q] = fma(acc[q], sv, hc.a[min(1 + q, 15)][j]);
+#pragma unroll
+  for (int q = 0; q < 4 * NG; ++q)
+    if (1 + q < w - 1) wrow[1 + q] = acc[q];
+}
+
 // ES weights of the chunk's particles (positions already staged); particles
 // cnt .. pad-1 get zero rows.  One item per (dimension, particle): the w window
 // weights by per-node Horner polynomials (edge nodes exactly), zeros elsewhere
 // in the tile row.  Starts and ends with __syncthreads().
-template <bool SPLIT, int RX, int RY, int RZ, int CH>
+template <int RX, int RY, int RZ, int CH>
 __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int pad, const Brick& g,
                                           const int T0[3], const Horner& hc) {
   __syncthreads();
   const double two_over_w = 2.0 / g.w;
   const double flo = g.odd ? -0.5 : 0.0;
   const int w = g.w;
-  const int ngroups = (w - 2 + 3) / 4;  // groups of 4 interior nodes (>= 1 for w >= 3)
-  // SPLIT: one item per (group, dim, particle) -- more parallelism for big CTAs;
-  // else one item per (dim, particle) looping over its groups.
-  const int ng = SPLIT ? ngroups : 1;
-  // group-major item order: a warp's lanes share (grp, d), so the Horner
-  // coefficient reads are warp-uniform (constant-cache broadcast)
-  const int per_g = 3 * pad;
-  for (int it = threadIdx.x; it < ng * per_g; it += blockDim.x) {
-    const int grp = it / per_g;
-    const int rem = it - grp * per_g;
-    const int d = rem / pad, p = rem - d * pad;
+  const int ng = (w - 2 + 3) / 4;  // groups of 4 interior nodes
+  // item = (dimension, particle): a warp's lanes share the dimension
+  for (int it = threadIdx.x; it < 3 * pad; it += blockDim.x) {
+    const int d = it / pad, p = it - d * pad;
     const int R = d == 0 ? RX : (d == 1 ? RY : (RZ + 7) / 8 * 8);
     double* row = d == 0 ? sm.px[p] : (d == 1 ? sm.py[p] : sm.pz[p]);
     if (p >= cnt) {
-      if (grp == 0)
-        for (int u = 0; u < R; ++u) row[u] = 0.0;
+      for (int u = 0; u < R; ++u) row[u] = 0.0;
       continue;
     }
     const int rel = sm.rel[p][d];
     const int T0d = d == 0 ? T0[0] : (d == 1 ? T0[1] : T0[2]);
     const double f = sm.xs[p][d] - (double)(rel + g.hw + T0d);  // x~ - anchor
-    if (grp == 0) {
-      for (int u = 0; u < rel; ++u) row[u] = 0.0;
-      for (int u = rel + w; u < R; ++u) row[u] = 0.0;
-      row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
-      row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
-    }
-    // interior nodes k0 .. k0+3 of a group: four independent Horner chains
+    for (int u = 0; u < rel; ++u) row[u] = 0.0;
+    for (int u = rel + w; u < R; ++u) row[u] = 0.0;
     const double sv = 2.0 * (f - flo) - 1.0;
-    for (int gg = SPLIT ? grp : 0; gg < (SPLIT ? grp + 1 : ngroups); ++gg) {
-      const int k0 = 1 + 4 * gg;
-      double acc[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = hc.a[min(k0 + q, 15)][kHornerDeg];
-#pragma unroll
-      for (int j = kHornerDeg - 1; j >= 0; --j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = fma(acc[q], sv, hc.a[min(k0 + q, 15)][j]);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (k0 + q < w - 1) row[rel + k0 + q] = acc[q];
+    switch (ng) {  // uniform
+      case 0: horner_row<0>(row + rel, f, sv, hc, g, two_over_w); break;
+      case 1: horner_row<1>(row + rel, f, sv, hc, g, two_over_w); break;
+      case 2: horner_row<2>(row + rel, f, sv, hc, g, two_over_w); break;
+      case 3: horner_row<3>(row + rel, f, sv, hc, g, two_over_w); break;
+      default: horner_row<4>(row + rel, f, sv, hc, g, two_over_w); break;
     }
   }
   __syncthreads();
@@ -217,7 +223,7 @@ struct SpreadCfg {
 };
 
 template <int RX, int RY, int RZ, bool HAS_S>
-__global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
+__global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, PIF_SPREAD_MINB)
     k_spread(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
              double s_uniform, const Sched Sc, Brick g,
              const __grid_constant__ Horner hc, double* __restrict__ grid) {
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
       stage_position(sm, q, xr, g, T0);
       if (HAS_S) sm.str[q] = s[base + q];
     }
-    stage_psi<false>(sm, cnt, pad, g, T0, hc);
+    stage_psi(sm, cnt, pad, g, T0, hc);
     for (int p0 = 0; p0 < pad; p0 += 4) {
       const int pl = p0 + tq;  // K index of this lane's A and B elements
       double b[C::ZT];
@@ -283,28 +289,6 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW)
         if (z < RZ && val != 0.0) atomicAdd(colp + wrapi(T0[2] + z, n), val * s_uniform);
       }
   }
-}
-
-// Interior nodes 1 .. 4 NG of one psi row by Horner, all 4 NG chains in one
-// pass (14 dependent steps instead of 14 NG: the FP64 pipe is shared with the
-// other warps' DMMAs, so each dependent step waits behind them).
-template <int NG>
-__device__ __forceinline__ void horner_row(double* wrow, double f, double sv, const Horner& hc,
-                                           const Brick& g, double two_over_w) {
-  const int w = g.w;
-  // edge nodes exactly (sqrt singularity at |t| = w/2), independent of the chains below
-  wrow[0] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
-  wrow[w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
-  double acc[4 * NG + 1];  // (+1: NG may be 0)
-#pragma unroll
-  for (int q = 0; q < 4 * NG; ++q) acc[q] = hc.a[min(1 + q, 15)][kHornerDeg];
-#pragma unroll
-  for (int j = kHornerDeg - 1; j >= 0; --j)
-#pragma unroll
-    for (int q = 0; q < 4 * NG; ++q) acc[q] = fma(acc[q], sv, hc.a[min(1 + q, 15)][j]);
-#pragma unroll
-  for (int q = 0; q < 4 * NG; ++q)
-    if (1 + q < w - 1) wrow[1 + q] = acc[q];
 }
 
 // ------------------------------------------------------------ interp+push --
