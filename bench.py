@@ -37,7 +37,9 @@ CASE = "landau"
 CONFIGS = {1: ("landau", 32, 1 << 21, 1e-12, 0.05),     # C2
            2: ("tsi", 32, 1 << 23, 1e-12, 0.05),        # C3
            3: ("penning", 64, 1 << 24, 1e-12, 0.003125),  # C4 (Boris push)
-           4: ("landau", 64, 1 << 26, 1e-7, 0.003125)}    # C5 fine propagator (1 GPU)
+           4: ("landau", 64, 1 << 26, 1e-7, 0.003125),    # C5 fine propagator (1 GPU)
+           5: ("landau", 64, 1 << 22, 1e-7, 0.003125),    # C5-reduced parareal fine propagator
+           6: ("landau", 64, 1 << 22, 1e-4, 0.05)}        # C5-reduced parareal coarse (PIF) propagator
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 SM_COUNT = 148

@@ -201,7 +201,7 @@ struct pif_ctx_s {
   size_t ws_bytes = 0;
   double *xA = nullptr, *vA = nullptr, *xB = nullptr, *vB = nullptr;
   int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *counts = nullptr,
-      *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr;
+      *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr, *spart = nullptr;
   int4 *sitems = nullptr, *iitems = nullptr;
   int64_t max_s = 1, max_i = 1;
   double *partials = nullptr, *red = nullptr;
@@ -242,6 +242,7 @@ size_t layout(pif_ctx c, char* base) {
   c->offsets = (int*)take((c->max_bins + 1) * sizeof(int));
   c->soff = (int*)take((c->max_bins + 1) * sizeof(int));
   c->ioff = (int*)take((c->max_bins + 1) * sizeof(int));
+  c->spart = (int*)take(3 * ((size_t)c->max_bins / 256 + 2) * sizeof(int));
   c->max_s = c->max_i = 1;
   for (int i = 0; i < 2; ++i) {
     const Plan& p = c->plan[i];
@@ -299,11 +300,17 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     // Small tiles waste fewer FMAs on padding but carry fewer particles per CTA;
     // below ~12 (w = 8) / ~8 (w = 5) particles per upsampled cell the per-CTA
     // overheads win, so the larger tiles are kept there (measured).
+#ifndef PIF_W8_PPC
+#define PIF_W8_PPC 12.0
+#endif
+#ifndef PIF_W5_PPC
+#define PIF_W5_PPC 8.0
+#endif
     const double ppc = (double)c->nloc / ((double)n * n * n);
     int RI[3], m[3] = {1, 1, 1};
-    if (w == 5 && ppc >= 8.0) { RI[0] = RI[1] = 6; RI[2] = 8; m[0] = m[1] = 2; }      // spread 8^3
+    if (w == 5 && ppc >= PIF_W5_PPC) { RI[0] = RI[1] = 6; RI[2] = 8; m[0] = m[1] = 2; }      // spread 8^3
     else if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
-    else if (w == 8 && ppc >= 12.0) { RI[0] = RI[1] = 10; RI[2] = 8; m[0] = m[1] = 3; }  // spread 16x16x8
+    else if (w == 8 && ppc >= PIF_W8_PPC) { RI[0] = RI[1] = 10; RI[2] = 8; m[0] = m[1] = 3; }  // spread 16x16x8
     else if (w <= 9) { RI[0] = RI[1] = RI[2] = 12; }
 #ifndef PIF_W13_TILE
 #define PIF_W13_TILE 1
@@ -434,7 +441,7 @@ pif_status ph_mark(pif_ctx c, int ph) {
 
 Sched sched_of(pif_ctx c, const Plan& p) {
   const int64_t M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
-  return Sched{c->offsets, c->soff, c->ioff, c->sitems, c->iitems, p.nbricks,
+  return Sched{c->offsets, c->soff, c->ioff, c->sitems, c->iitems, c->spart, p.nbricks,
                sched_max_s(p.nbricks, M, c->nloc), sched_max_i(p.nbricks, c->nloc)};
 }
 
@@ -1179,13 +1186,13 @@ pif_status pif_finalize(pif_ctx c) {
 static pif_status debug_sched(pif_ctx c, const Plan& p, int64_t n, int** counts, Sched& S) {
   const int64_t K = p.nbricks, M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
   const int64_t ms = sched_max_s(K, M, n), mi = sched_max_i(K, n);
-  const size_t ints = K + 3 * (K + 1);
+  const size_t ints = K + 3 * (K + 1) + 3 * ((size_t)K / 256 + 2);
   char* buf = nullptr;
   CU(cudaMalloc(&buf, ints * sizeof(int) + 16 + (ms + mi) * sizeof(int4)));
   int* ib = (int*)buf;
   *counts = ib;
   int4* items = (int4*)(((uintptr_t)(ib + ints) + 15) & ~(uintptr_t)15);
-  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, items, items + ms, K, ms, mi};
+  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, items, items + ms, ib + 4 * K + 3, K, ms, mi};
   return PIF_OK;
 }
 pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, const double* s,

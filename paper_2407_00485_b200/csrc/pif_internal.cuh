@@ -145,8 +145,14 @@ struct Sched {
   int* ioff;     // [nkeys + 1]
   int4* sitems;  // [max_s]
   int4* iitems;  // [max_i]
+  int* part;     // [3 * sched_part_blocks(nkeys, M)] scan scratch
   int64_t nkeys, max_s, max_i;
 };
+// blocks of the schedule scan (256 bricks each; >= 1)
+inline unsigned nblk_sched(int64_t nkeys, int64_t M) {
+  const int64_t b = (nkeys / M + 255) / 256;
+  return (unsigned)(b < 1 ? 1 : b);
+}
 inline int64_t sched_max_s(int64_t nkeys, int64_t M, int64_t n) { return nkeys / M + n / kSpreadItem + 1; }
 inline int64_t sched_max_i(int64_t nkeys, int64_t n) { return nkeys + n / kInterpItem + 1; }
 
@@ -154,7 +160,6 @@ inline int64_t sched_max_i(int64_t nkeys, int64_t n) { return nkeys + n / kInter
 // All launchers enqueue on `st` and return cudaGetLastError().
 cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const Brick& g, int* key,
                              int* rank, int* counts, cudaStream_t st);
-cudaError_t launch_scan(const int* counts, int* offsets, int64_t nbins, cudaStream_t st);
 cudaError_t launch_schedule(const int* counts, const Sched& S, int M, cudaStream_t st);
 cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,
                                   int64_t stride, int64_t n, const int* key, const int* rank,

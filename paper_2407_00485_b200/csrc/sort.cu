@@ -33,72 +33,84 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
   rank[j] = base + __popc(peers & ((1u << lane) - 1u));
 }
 
-// Exclusive scan of counts[0..nbins) into offsets[0..nbins] with one CTA of
-// 1024 threads (nbins <= 2^20): per-thread serial chunk + block scan of sums.
-__global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ counts,
-                                               int* __restrict__ offsets, int64_t nbins) {
-  __shared__ int warp_sums[32];
-  const int T = blockDim.x, t = threadIdx.x;
-  const int64_t per = (nbins + T - 1) / T;
-  const int64_t lo = t * per, hi = min(nbins, lo + per);
-  int local = 0;
-  for (int64_t i = lo; i < hi; ++i) local += counts[i];
-  // inclusive scan of `local` across the block
-  int lane = t & 31, wid = t >> 5;
-  int v = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int u = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += u;
+// Exclusive scans of (counts, spread items, interp items) over keys, three
+// passes over bricks (one thread = one brick = M consecutive keys, blocks of
+// kSchedT bricks): per-block totals, one-CTA scan of the block totals, per-block
+// scan + writes.  offsets[k] / ioff[k]: first particle / interp item of key k;
+// soff[brick key]: first spread item of the brick (soff[k], k not a brick's first
+// key: end of its brick's items); [nkeys] = totals.
+constexpr int kSchedT = 256;
+
+__device__ __forceinline__ void brick_sums(const int* __restrict__ counts, int64_t i0, int M,
+                                           int a[3]) {
+  int bs = 0, it = 0;
+  for (int m = 0; m < M; ++m) {
+    const int c = counts[i0 + m];
+    bs += c;
+    it += (c + kInterpItem - 1) / kInterpItem;
   }
-  if (lane == 31) warp_sums[wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    int w = (lane < (T >> 5)) ? warp_sums[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int u = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += u;
-    }
-    warp_sums[lane] = w;
-  }
-  __syncthreads();
-  int excl = v - local + (wid > 0 ? warp_sums[wid - 1] : 0);
-  for (int64_t i = lo; i < hi; ++i) {
-    offsets[i] = excl;
-    excl += counts[i];
-  }
-  if (t == T - 1) offsets[nbins] = excl;
+  a[0] = bs;
+  a[1] = (bs + kSpreadItem - 1) / kSpreadItem;
+  a[2] = it;
 }
 
-// Exclusive scans of (counts, spread items, interp items) over keys in one CTA;
-// per-thread chunks are whole bricks (multiples of M keys).
-__global__ void __launch_bounds__(1024) k_schedule_scan(const int* __restrict__ counts, Sched S,
-                                                        int M) {
-  __shared__ int sh[3][32];
-  const int T = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const int64_t nk = S.nkeys;
-  int64_t per = (nk + T - 1) / T;
-  per = (per + M - 1) / M * M;
-  const int64_t lo = min(nk, t * per), hi = min(nk, lo + per);
-  int a[3] = {0, 0, 0};
-  for (int64_t i = lo; i < hi; i += M) {
-    int bs = 0;
-    for (int m = 0; m < M; ++m) {
-      int c = counts[i + m];
-      a[0] += c;
-      a[2] += (c + kInterpItem - 1) / kInterpItem;
-      bs += c;
-    }
-    a[1] += (bs + kSpreadItem - 1) / kSpreadItem;
-  }
+// Block-wide exclusive scan of three ints (blockDim.x == kSchedT); returns the
+// block totals in tot.
+__device__ __forceinline__ void block_scan3(const int a[3], int ex[3], int tot[3]) {
+  __shared__ int sh[3][kSchedT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int incl[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     int v = a[q];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int u = __shfl_up_sync(0xffffffffu, v, o);
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    incl[q] = v;
+    if (lane == 31) sh[q][wid] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kSchedT / 32; ++w) {
+      const int x = sh[q][w];
+      if (w < wid) before += x;
+      all += x;
+    }
+    ex[q] = incl[q] - a[q] + before;
+    tot[q] = all;
+  }
+}
+
+__global__ void __launch_bounds__(kSchedT) k_sched_reduce(const int* __restrict__ counts, Sched S,
+                                                          int M) {
+  const int64_t nb = S.nkeys / M, br = blockIdx.x * (int64_t)kSchedT + threadIdx.x;
+  int a[3] = {0, 0, 0}, ex[3], tot[3];
+  if (br < nb) brick_sums(counts, br * M, M, a);
+  block_scan3(a, ex, tot);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) S.part[3 * blockIdx.x + q] = tot[q];
+}
+
+// In place: part[3 b + q] <- sum of part[3 b' + q] over b' < b (one CTA).
+__global__ void __launch_bounds__(1024) k_sched_partials(Sched S, int nblk) {
+  __shared__ int sh[3][32];
+  const int T = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int per = (nblk + T - 1) / T, lo = min(nblk, t * per), hi = min(nblk, lo + per);
+  int a[3] = {0, 0, 0};
+  for (int i = lo; i < hi; ++i)
+    for (int q = 0; q < 3; ++q) a[q] += S.part[3 * i + q];
+  int incl[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int v = a[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
       if (lane >= o) v += u;
     }
     incl[q] = v;
@@ -111,7 +123,7 @@ __global__ void __launch_bounds__(1024) k_schedule_scan(const int* __restrict__ 
       int w = lane < (T >> 5) ? sh[q][lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int u = __shfl_up_sync(0xffffffffu, w, o);
+        const int u = __shfl_up_sync(0xffffffffu, w, o);
         if (lane >= o) w += u;
       }
       sh[q][lane] = w;
@@ -121,21 +133,35 @@ __global__ void __launch_bounds__(1024) k_schedule_scan(const int* __restrict__ 
   int ex[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) ex[q] = incl[q] - a[q] + (wid > 0 ? sh[q][wid - 1] : 0);
-  for (int64_t i = lo; i < hi; i += M) {
-    int bs = 0;
-    for (int m = 0; m < M; ++m) bs += counts[i + m];
-    S.soff[i] = ex[1];
-    ex[1] += (bs + kSpreadItem - 1) / kSpreadItem;
-    for (int m = 0; m < M; ++m) {
-      int c = counts[i + m];
-      S.offsets[i + m] = ex[0];
-      S.ioff[i + m] = ex[2];
-      if (m) S.soff[i + m] = ex[1];
-      ex[0] += c;
-      ex[2] += (c + kInterpItem - 1) / kInterpItem;
+  for (int i = lo; i < hi; ++i)
+    for (int q = 0; q < 3; ++q) {
+      const int x = S.part[3 * i + q];
+      S.part[3 * i + q] = ex[q];
+      ex[q] += x;
     }
+}
+
+__global__ void __launch_bounds__(kSchedT) k_sched_apply(const int* __restrict__ counts, Sched S,
+                                                         int M) {
+  const int64_t nk = S.nkeys, nb = nk / M, br = blockIdx.x * (int64_t)kSchedT + threadIdx.x;
+  int a[3] = {0, 0, 0}, ex[3], tot[3];
+  if (br < nb) brick_sums(counts, br * M, M, a);
+  block_scan3(a, ex, tot);
+  if (br >= nb) return;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) ex[q] += S.part[3 * blockIdx.x + q];
+  const int64_t i = br * M;
+  S.soff[i] = ex[1];
+  ex[1] += a[1];
+  for (int m = 0; m < M; ++m) {
+    const int c = counts[i + m];
+    S.offsets[i + m] = ex[0];
+    S.ioff[i + m] = ex[2];
+    if (m) S.soff[i + m] = ex[1];
+    ex[0] += c;
+    ex[2] += (c + kInterpItem - 1) / kInterpItem;
   }
-  if (t == T - 1) {
+  if (br == nb - 1) {
     S.offsets[nk] = ex[0];
     S.soff[nk] = ex[1];
     S.ioff[nk] = ex[2];
@@ -202,12 +228,11 @@ cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const B
   if (n > 0) k_bin_count<<<nblk(n, 256), 256, 0, st>>>(x, stride, n, g, key, rank, counts);
   return cudaGetLastError();
 }
-cudaError_t launch_scan(const int* counts, int* offsets, int64_t nbins, cudaStream_t st) {
-  k_scan<<<1, 1024, 0, st>>>(counts, offsets, nbins);
-  return cudaGetLastError();
-}
 cudaError_t launch_schedule(const int* counts, const Sched& S, int M, cudaStream_t st) {
-  k_schedule_scan<<<1, 1024, 0, st>>>(counts, S, M);
+  const unsigned nsb = nblk_sched(S.nkeys, M);
+  k_sched_reduce<<<nsb, kSchedT, 0, st>>>(counts, S, M);
+  k_sched_partials<<<1, 1024, 0, st>>>(S, (int)nsb);
+  k_sched_apply<<<nsb, kSchedT, 0, st>>>(counts, S, M);
   k_schedule_fill<<<nblk(S.nkeys, 256), 256, 0, st>>>(S, M);
   return cudaGetLastError();
 }

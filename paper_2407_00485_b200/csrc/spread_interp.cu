@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, PIF_SPREAD_MIN
 // values per particle inside the warp, and the warp pushes its own particles.
 //
 // Persistent and warp-specialised: one producer warp streams the g tiles of the
-// CTA's items (blockIdx.x, + gridDim.x, ...) into a double buffer with cp.async,
-// completion signalled on mbarriers full[b]; NW consumer warps walk the CTA's
+// CTA's items (blockIdx.x, + gridDim.x, ...) into a ring of NBUF tile buffers
+// with cp.async, completion signalled on mbarriers full[b]; NW consumer warps walk the CTA's
 // concatenated m-tile sequence round-robin, each with its own x, v cp.async
 // double buffer and psi rows (24 lanes = 8 particles x 3 dimensions, Horner
 // groups warp-uniform), and release a tile buffer (empty[b]) once past its item.
@@ -324,11 +324,16 @@ struct InterpCfg {
   static constexpr int OY = 8 * SX + 1, OZ = OY + 8 * SY + 1;
   static constexpr int WP = OZ + 8 * SZ;   // psi doubles per warp (even: 16-byte aligned)
   static constexpr int GB = KS * NT * 3 * 32;  // doubles per g-tile buffer
-  // consumer warps: as many as fit (<= 16) next to the double-buffered tile in
-  // the 227 KB of dynamic shared memory a CTA may use
-  static constexpr int BUDGET = (232448 - 64) / 8 - 2 * GB;
+  // consumer warps: as many as fit (<= 16) next to a double-buffered tile in
+  // the 227 KB of dynamic shared memory a CTA may use; then as many tile
+  // buffers as fit (<= 8: small tiles carry few particles, so the producer must
+  // run several items ahead of the consumers)
+  static constexpr int BYTES = 232448 - 16 * 8;  // minus the mbarriers
+  static constexpr int BUDGET = BYTES / 8 - 2 * GB;
   static constexpr int NWFIT = BUDGET / (WP + 96);
   static constexpr int NW = NWFIT < 16 ? NWFIT : 16;
+  static constexpr int NBFIT = (BYTES / 8 - NW * (WP + 96)) / GB;
+  static constexpr int NBUF = NBFIT < 8 ? NBFIT : 8;
   static_assert(NC % 4 == 0, "tile columns must be a multiple of 4");
   static_assert(OZ % 2 == 0 && WP % 2 == 0, "pz rows are read as double2");
   static_assert(NW >= 4, "tile too large for the persistent interpolation kernel");
@@ -337,10 +342,10 @@ struct InterpCfg {
 template <int RX, int RY, int RZ>
 struct InterpSmem {
   using C = InterpCfg<RX, RY, RZ>;
-  double gB[2][C::KS][C::NT][3][32];  // B fragments, double-buffered over items
-  double psi[C::NW][C::WP];           // per-warp psi rows
-  double xv[C::NW][2][6][8];          // per-warp x, v double buffer (cp.async)
-  unsigned long long full[2], empty[2];
+  double gB[C::NBUF][C::KS][C::NT][3][32];  // B fragments, ring of tile buffers
+  double psi[C::NW][C::WP];                 // per-warp psi rows
+  double xv[C::NW][2][6][8];                // per-warp x, v double buffer (cp.async)
+  unsigned long long full[C::NBUF], empty[C::NBUF];
 };
 
 // An interpolation item of this CTA (the k-th: item blockIdx.x + k gridDim.x)
@@ -381,16 +386,15 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n = g.n;
   const int64_t n3 = (int64_t)n * n * n;
-  if (threadIdx.x == 0) {
-    mbar_init(&S.full[0], 32);
-    mbar_init(&S.full[1], 32);
-    mbar_init(&S.empty[0], C::NW);
-    mbar_init(&S.empty[1], C::NW);
-  }
+  if (threadIdx.x == 0)
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(&S.full[b], 32);
+      mbar_init(&S.empty[b], C::NW);
+    }
   __syncthreads();
 
   if (wid == C::NW) {
-    // ---- producer: g tile of item k -> gB[k & 1], stored lane-permuted:
+    // ---- producer: g tile of item k -> gB[k % NBUF], stored lane-permuted:
     // B[t][g] = g_d[c = 4 ks + t][z = 8 nt + g] at gB[.][ks][nt][d][e],
     // e = 16 (g >> 2) + 4 t + (g & 3): each half-warp of a fragment read (g = 0..3
     // or 4..7) hits 16 distinct 8-byte bank slots, and the stores come in
@@ -399,8 +403,8 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
     const int eoff = (h << 4) | (t << 2) | zq;
     ItemCursor it;
     for (it.k = 0; it.k < nitems; ++it.k) {
-      const int b = it.k & 1;
-      if (it.k >= 2) mbar_wait(&S.empty[b], ((it.k >> 1) - 1) & 1);
+      const int b = it.k % C::NBUF;
+      if (it.k >= C::NBUF) mbar_wait(&S.empty[b], (it.k / C::NBUF - 1) & 1);
       cursor_load(it, g, Sc);
       int gz[C::NT];
       bool zin[C::NT];
@@ -453,9 +457,9 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
   auto advance = [&](ItemCursor& it, int q, bool release) {
     while (it.k < nitems && q >= it.base + it.m) {
       if (release) {
-        mbar_wait(&S.full[it.k & 1], (it.k >> 1) & 1);
+        mbar_wait(&S.full[it.k % C::NBUF], (it.k / C::NBUF) & 1);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[it.k & 1]);
+        if (lane == 0) mbar_arrive(&S.empty[it.k % C::NBUF]);
       }
       it.base += it.m;
       if (++it.k < nitems) cursor_load(it, g, Sc);
@@ -516,8 +520,8 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
     stage(buf, cnt);
-    const int tb = c.k & 1;
-    mbar_wait(&S.full[tb], (c.k >> 1) & 1);  // g tile of this item landed
+    const int tb = c.k % C::NBUF;
+    mbar_wait(&S.full[tb], (c.k / C::NBUF) & 1);  // g tile of this item landed
     __syncwarp();                            // psi rows visible to the warp
     double acc[C::NT][3][2];
 #pragma unroll
