@@ -334,6 +334,9 @@ struct InterpCfg {
   static constexpr int NW = NWFIT < 16 ? NWFIT : 16;
   static constexpr int NBFIT = (BYTES / 8 - NW * (WP + 96)) / GB;
   static constexpr int NBUF = NBFIT < 8 ? NBFIT : 8;
+  // producer warps: small tiles carry few particles per loaded byte, so one
+  // warp's copy issue rate would bound the kernel; they split the k steps
+  static constexpr int NP = GB * 8 <= 24576 ? 4 : 1;
   static_assert(NC % 4 == 0, "tile columns must be a multiple of 4");
   static_assert(OZ % 2 == 0 && WP % 2 == 0, "pz rows are read as double2");
   static_assert(NW >= 4, "tile too large for the persistent interpolation kernel");
@@ -371,7 +374,7 @@ __device__ __forceinline__ void cursor_load(ItemCursor& it, const Brick& g, cons
 }
 
 template <int RX, int RY, int RZ>
-__global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
+__global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX, RY, RZ>::NP), 1)
     k_interp_push(const double* __restrict__ grid3, double* __restrict__ x,
                   double* __restrict__ v, int64_t stride, const int* __restrict__ id,
                   double* __restrict__ Eout, const Sched Sc, Brick g,
@@ -388,12 +391,12 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
   const int64_t n3 = (int64_t)n * n * n;
   if (threadIdx.x == 0)
     for (int b = 0; b < C::NBUF; ++b) {
-      mbar_init(&S.full[b], 32);
+      mbar_init(&S.full[b], 32 * C::NP);
       mbar_init(&S.empty[b], C::NW);
     }
   __syncthreads();
 
-  if (wid == C::NW) {
+  if (wid >= C::NW) {
     // ---- producer: g tile of item k -> gB[k % NBUF], stored lane-permuted:
     // B[t][g] = g_d[c = 4 ks + t][z = 8 nt + g] at gB[.][ks][nt][d][e],
     // e = 16 (g >> 2) + 4 t + (g & 3): each half-warp of a fragment read (g = 0..3
@@ -415,8 +418,9 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
         gz[nt] = z < 0 ? z + n : (z >= n ? z - n : z);
         zin[nt] = zl < RZ;
       }
-      int cx = t % RX, cy = t / RX;
-      for (int ks = 0; ks < C::KS; ++ks) {
+      const int pw = wid - C::NW;  // this producer's k steps: pw, pw + NP, ...
+      int cx = (4 * pw + t) % RX, cy = (4 * pw + t) / RX;
+      for (int ks = pw; ks < C::KS; ks += C::NP) {
         int gx = it.T0[0] + cx, gy = it.T0[1] + cy;
         gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
         gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
@@ -426,7 +430,8 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + 1), 1)
 #pragma unroll
           for (int d = 0; d < 3; ++d)
             cp_async8_zfill(&S.gB[b][ks][nt][d][eoff], src + d * n3 + gz[nt], zin[nt]);
-        cx += 4;
+        cx += (4 * C::NP) % RX;
+        cy += (4 * C::NP) / RX;
         if (cx >= RX) {
           cx -= RX;
           cy += 1;
@@ -629,7 +634,7 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
                                  int64_t stride, const int* id, double* Eout, const Sched& offsets,
                                  const Brick& g, const Horner& hc, const PushArgs& P,
                                  cudaStream_t st) {
-  const int T = 32 * (InterpCfg<A, B, Cz>::NW + 1);
+  const int T = 32 * (InterpCfg<A, B, Cz>::NW + InterpCfg<A, B, Cz>::NP);
   const size_t smem = sizeof(InterpSmem<A, B, Cz>);
   static int ctas = 0;  // persistent grid: SMs x resident CTAs per SM
   if (!ctas) {
