@@ -152,26 +152,53 @@ __device__ __forceinline__ void stage_position(Psi<RX, RY, RZ, CH>& sm, int tid,
   }
 }
 
-// Interior nodes 1 .. 4 NG of one psi row by Horner, all 4 NG chains in one
-// pass (14 dependent steps instead of 14 NG: the FP64 pipe is shared with the
-// other warps' DMMAs, so each dependent step waits behind them).
-template <int NG>
-__device__ __forceinline__ void horner_row(double* wrow, double f, double sv, const Horner& hc,
-                                           const Brick& g, double two_over_w) {
-  const int w = g.w;
-  // edge nodes exactly (sqrt singularity at |t| = w/2), independent of the chains below
-  wrow[0] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
-  wrow[w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
-  double acc[4 * NG + 1];  // (+1: NG may be 0)
+// One psi row: the w window weights of a particle at row[rel .. rel + w).  Edge
+// nodes exactly (sqrt singularity at |t| = w/2).  Interior nodes by the per-node
+// polynomials P_k(s) in s = 2 (f - flo) - 1, using the evenness of the ES kernel:
+// with hw = (w - 1) / 2, node w-1-k at s equals node k at -s, so one split
+// P_k(s) = E_k(s^2) + s O_k(s^2) gives both nodes of a pair (7 dependent steps,
+// ~15 FMAs per pair instead of 14 steps and 30 FMAs); the centre node of an odd
+// w is even in s (E only).  All pairs are evaluated in one pass: the FP64 pipe
+// is shared with the DMMAs, so dependent steps, not FMAs, set the latency.
+template <int NPAIR, bool CENTER>
+__device__ __forceinline__ void horner_sym(double* row, int rel, double f, double sv,
+                                           const Horner& hc, const Brick& g, double two_over_w) {
+  constexpr int w = 2 * NPAIR + 2 + (CENTER ? 1 : 0);
+  constexpr int NE = NPAIR + (CENTER ? 1 : 0);
+  row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
+  row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+  const double s2 = sv * sv;
+  double e[NE + 1], o[NPAIR + 1];  // (+1: may be empty)
 #pragma unroll
-  for (int q = 0; q < 4 * NG; ++q) acc[q] = hc.a[min(1 + q, 15)][kHornerDeg];
+  for (int i = 0; i < NE; ++i) e[i] = hc.a[1 + i][kHornerDeg];
 #pragma unroll
-  for (int j = kHornerDeg - 1; j >= 0; --j)
+  for (int i = 0; i < NPAIR; ++i) o[i] = hc.a[1 + i][kHornerDeg - 1];
 #pragma unroll
-    for (int q = 0; q < 4 * NG; ++q) acc[q] = fma(acc[q], sv, hc.a[min(1 + q, 15)][j]);
+  for (int j = kHornerDeg / 2 - 1; j >= 0; --j) {
 #pragma unroll
-  for (int q = 0; q < 4 * NG; ++q)
-    if (1 + q < w - 1) wrow[1 + q] = acc[q];
+    for (int i = 0; i < NE; ++i) e[i] = fma(e[i], s2, hc.a[1 + i][2 * j]);
+    if (j < kHornerDeg / 2 - 1)
+#pragma unroll
+      for (int i = 0; i < NPAIR; ++i) o[i] = fma(o[i], s2, hc.a[1 + i][2 * j + 1]);
+  }
+#pragma unroll
+  for (int i = 0; i < NPAIR; ++i) {
+    row[rel + 1 + i] = fma(sv, o[i], e[i]);
+    row[rel + w - 2 - i] = fma(-sv, o[i], e[i]);
+  }
+  if (CENTER) row[rel + 1 + NPAIR] = e[NPAIR];
+}
+
+__device__ __forceinline__ void psi_row(double* row, int rel, double f, double sv,
+                                        const Horner& hc, const Brick& g, double two_over_w) {
+  switch (g.w) {  // uniform
+#define PIF_W(W) \
+  case W: horner_sym<(W - 2) / 2, (W & 1) == 1>(row, rel, f, sv, hc, g, two_over_w); break;
+    PIF_W(2) PIF_W(3) PIF_W(4) PIF_W(5) PIF_W(6) PIF_W(7) PIF_W(8) PIF_W(9)
+    PIF_W(10) PIF_W(11) PIF_W(12) PIF_W(13) PIF_W(14) PIF_W(15) PIF_W(16)
+#undef PIF_W
+    default: break;
+  }
 }
 
 // ES weights of the chunk's particles (positions already staged); particles
@@ -185,7 +212,6 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
   const double two_over_w = 2.0 / g.w;
   const double flo = g.odd ? -0.5 : 0.0;
   const int w = g.w;
-  const int ng = (w - 2 + 3) / 4;  // groups of 4 interior nodes
   // item = (dimension, particle): a warp's lanes share the dimension
   for (int it = threadIdx.x; it < 3 * pad; it += blockDim.x) {
     const int d = it / pad, p = it - d * pad;
@@ -201,13 +227,7 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
     for (int u = 0; u < rel; ++u) row[u] = 0.0;
     for (int u = rel + w; u < R; ++u) row[u] = 0.0;
     const double sv = 2.0 * (f - flo) - 1.0;
-    switch (ng) {  // uniform
-      case 0: horner_row<0>(row + rel, f, sv, hc, g, two_over_w); break;
-      case 1: horner_row<1>(row + rel, f, sv, hc, g, two_over_w); break;
-      case 2: horner_row<2>(row + rel, f, sv, hc, g, two_over_w); break;
-      case 3: horner_row<3>(row + rel, f, sv, hc, g, two_over_w); break;
-      default: horner_row<4>(row + rel, f, sv, hc, g, two_over_w); break;
-    }
+    psi_row(row, rel, f, sv, hc, g, two_over_w);
   }
   __syncthreads();
 }
@@ -505,13 +525,7 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
         const double f = xs - (double)a;
         double* wrow = row + (a - g.hw - T0d);
         const double sv = 2.0 * (f - flo) - 1.0;
-        switch ((w - 2 + 3) / 4) {  // warp-uniform
-          case 0: horner_row<0>(wrow, f, sv, hc, g, two_over_w); break;
-          case 1: horner_row<1>(wrow, f, sv, hc, g, two_over_w); break;
-          case 2: horner_row<2>(wrow, f, sv, hc, g, two_over_w); break;
-          case 3: horner_row<3>(wrow, f, sv, hc, g, two_over_w); break;
-          default: horner_row<4>(wrow, f, sv, hc, g, two_over_w); break;
-        }
+        psi_row(wrow, 0, f, sv, hc, g, two_over_w);
       }
     }
   };
