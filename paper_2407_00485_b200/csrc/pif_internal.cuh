@@ -50,8 +50,9 @@ struct Brick {
 // w) the window node k (grid point a - hw + k) has weight psi(k - hw - f) =
 // P_k(s), s = 2 (f - f_lo) - 1 in [-1, 1], with P_k a degree-kHornerDeg
 // Chebyshev interpolant in monomial form (max error ~5e-15 on interior nodes).
-// The two edge nodes k = 0, w-1 carry the sqrt singularity of psi at |t| = w/2
-// and are evaluated exactly.  Passed by value as a __grid_constant__ kernel
+// The two edge nodes k = 0, w-1 carry the sqrt singularity of psi at |t| = w/2;
+// their fit error is ~0.05 eps (w >= 5), below the NUFFT error budget, so they
+// are polynomials too (exact for w <= 4, spread_interp.cu:horner_sym).  Passed by value as a __grid_constant__ kernel
 // parameter: every lane of a warp reads the same coefficient (constant cache).
 constexpr int kHornerDeg = 14;
 struct Horner {

@@ -152,8 +152,7 @@ __device__ __forceinline__ void stage_position(Psi<RX, RY, RZ, CH>& sm, int tid,
   }
 }
 
-// One psi row: the w window weights of a particle at row[rel .. rel + w).  Edge
-// nodes exactly (sqrt singularity at |t| = w/2).  Interior nodes by the per-node
+// One psi row: the w window weights of a particle at row[rel .. rel + w), by the per-node
 // polynomials P_k(s) in s = 2 (f - flo) - 1, using the evenness of the ES kernel:
 // with hw = (w - 1) / 2, node w-1-k at s equals node k at -s, so one split
 // P_k(s) = E_k(s^2) + s O_k(s^2) gives both nodes of a pair (7 dependent steps,
@@ -164,29 +163,40 @@ template <int NPAIR, bool CENTER>
 __device__ __forceinline__ void horner_sym(double* row, int rel, double f, double sv,
                                            const Horner& hc, const Brick& g, double two_over_w) {
   constexpr int w = 2 * NPAIR + 2 + (CENTER ? 1 : 0);
-  constexpr int NE = NPAIR + (CENTER ? 1 : 0);
-  row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
-  row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+  // Edge nodes: their polynomial fit error is ~0.05 eps for w >= 5 (degree 14,
+  // e.g. 5e-14 at w = 13, 4e-9 at w = 8, 3e-6 at w = 5), so they join the pairs;
+  // small widths (w <= 4, fit error up to 0.25 eps) evaluate them exactly.
+#ifdef PIF_EXACT_EDGES
+  constexpr int P0 = 1;
+#else
+  constexpr int P0 = w <= 4 ? 1 : 0;
+#endif
+  if (P0) {
+    row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
+    row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+  }
+  constexpr int NP = NPAIR + 1 - P0;         // polynomial pairs: nodes (P0 + i, w - 1 - P0 - i)
+  constexpr int NE = NP + (CENTER ? 1 : 0);  // even parts (+ the centre node of an odd w)
   const double s2 = sv * sv;
-  double e[NE + 1], o[NPAIR + 1];  // (+1: may be empty)
+  double e[NE + 1], o[NP + 1];  // (+1: may be empty)
 #pragma unroll
-  for (int i = 0; i < NE; ++i) e[i] = hc.a[1 + i][kHornerDeg];
+  for (int i = 0; i < NE; ++i) e[i] = hc.a[P0 + i][kHornerDeg];
 #pragma unroll
-  for (int i = 0; i < NPAIR; ++i) o[i] = hc.a[1 + i][kHornerDeg - 1];
+  for (int i = 0; i < NP; ++i) o[i] = hc.a[P0 + i][kHornerDeg - 1];
 #pragma unroll
   for (int j = kHornerDeg / 2 - 1; j >= 0; --j) {
 #pragma unroll
-    for (int i = 0; i < NE; ++i) e[i] = fma(e[i], s2, hc.a[1 + i][2 * j]);
+    for (int i = 0; i < NE; ++i) e[i] = fma(e[i], s2, hc.a[P0 + i][2 * j]);
     if (j < kHornerDeg / 2 - 1)
 #pragma unroll
-      for (int i = 0; i < NPAIR; ++i) o[i] = fma(o[i], s2, hc.a[1 + i][2 * j + 1]);
+      for (int i = 0; i < NP; ++i) o[i] = fma(o[i], s2, hc.a[P0 + i][2 * j + 1]);
   }
 #pragma unroll
-  for (int i = 0; i < NPAIR; ++i) {
-    row[rel + 1 + i] = fma(sv, o[i], e[i]);
-    row[rel + w - 2 - i] = fma(-sv, o[i], e[i]);
+  for (int i = 0; i < NP; ++i) {
+    row[rel + P0 + i] = fma(sv, o[i], e[i]);
+    row[rel + w - 1 - P0 - i] = fma(-sv, o[i], e[i]);
   }
-  if (CENTER) row[rel + 1 + NPAIR] = e[NPAIR];
+  if (CENTER) row[rel + P0 + NP] = e[NP];
 }
 
 __device__ __forceinline__ void psi_row(double* row, int rel, double f, double sv,
