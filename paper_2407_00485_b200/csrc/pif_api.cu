@@ -201,7 +201,7 @@ struct pif_ctx_s {
   size_t ws_bytes = 0;
   double *xA = nullptr, *vA = nullptr, *xB = nullptr, *vB = nullptr;
   int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *counts = nullptr,
-      *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr, *spart = nullptr;
+      *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr, *moff = nullptr, *spart = nullptr;
   int4 *sitems = nullptr, *iitems = nullptr;
   int64_t max_s = 1, max_i = 1;
   double *partials = nullptr, *red = nullptr;
@@ -242,7 +242,8 @@ size_t layout(pif_ctx c, char* base) {
   c->offsets = (int*)take((c->max_bins + 1) * sizeof(int));
   c->soff = (int*)take((c->max_bins + 1) * sizeof(int));
   c->ioff = (int*)take((c->max_bins + 1) * sizeof(int));
-  c->spart = (int*)take(3 * ((size_t)c->max_bins / 256 + 2) * sizeof(int));
+  c->moff = (int*)take((c->max_bins + 1) * sizeof(int));
+  c->spart = (int*)take(4 * ((size_t)c->max_bins / 256 + 2) * sizeof(int));
   c->max_s = c->max_i = 1;
   for (int i = 0; i < 2; ++i) {
     const Plan& p = c->plan[i];
@@ -441,7 +442,7 @@ pif_status ph_mark(pif_ctx c, int ph) {
 
 Sched sched_of(pif_ctx c, const Plan& p) {
   const int64_t M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
-  return Sched{c->offsets, c->soff, c->ioff, c->sitems, c->iitems, c->spart, p.nbricks,
+  return Sched{c->offsets, c->soff, c->ioff, c->moff, c->sitems, c->iitems, c->spart, p.nbricks,
                sched_max_s(p.nbricks, M, c->nloc), sched_max_i(p.nbricks, c->nloc)};
 }
 
@@ -1186,13 +1187,14 @@ pif_status pif_finalize(pif_ctx c) {
 static pif_status debug_sched(pif_ctx c, const Plan& p, int64_t n, int** counts, Sched& S) {
   const int64_t K = p.nbricks, M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
   const int64_t ms = sched_max_s(K, M, n), mi = sched_max_i(K, n);
-  const size_t ints = K + 3 * (K + 1) + 3 * ((size_t)K / 256 + 2);
+  const size_t ints = K + 4 * (K + 1) + 4 * ((size_t)K / 256 + 2);
   char* buf = nullptr;
   CU(cudaMalloc(&buf, ints * sizeof(int) + 16 + (ms + mi) * sizeof(int4)));
   int* ib = (int*)buf;
   *counts = ib;
   int4* items = (int4*)(((uintptr_t)(ib + ints) + 15) & ~(uintptr_t)15);
-  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, items, items + ms, ib + 4 * K + 3, K, ms, mi};
+  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, ib + 4 * K + 3, items, items + ms, ib + 5 * K + 4,
+            K, ms, mi};
   return PIF_OK;
 }
 pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, const double* s,

@@ -136,7 +136,8 @@ __device__ __forceinline__ void push_particle(double& x0, double& x1, double& x2
 // arrays (offsets over sub-brick keys) cut into work items of at most kSpreadItem
 // (spread, per brick) / kInterpItem (interp, per sub-brick) particles, so a
 // crowded brick (e.g. the Penning cloud) is shared by several CTAs.  Item =
-// {brick or key, start, end, 0}; *_off are exclusive prefix sums over keys
+// {brick, start, end, 0} (spread) / {key, start, end, first m-tile} (interp);
+// *_off are exclusive prefix sums over keys
 // (spread items attributed to the first key of their brick); totals at [nkeys].
 constexpr int kSpreadItem = 4096;
 constexpr int kInterpItem = 1024;
@@ -144,9 +145,10 @@ struct Sched {
   int* offsets;  // [nkeys + 1]
   int* soff;     // [nkeys + 1]
   int* ioff;     // [nkeys + 1]
+  int* moff;     // [nkeys + 1] first m-tile (8 particles) of each key
   int4* sitems;  // [max_s]
   int4* iitems;  // [max_i]
-  int* part;     // [3 * sched_part_blocks(nkeys, M)] scan scratch
+  int* part;     // [4 * nblk_sched(nkeys, M)] scan scratch
   int64_t nkeys, max_s, max_i;
 };
 // blocks of the schedule scan (256 bricks each; >= 1)

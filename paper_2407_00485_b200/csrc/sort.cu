@@ -33,35 +33,46 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
   rank[j] = base + __popc(peers & ((1u << lane) - 1u));
 }
 
-// Exclusive scans of (counts, spread items, interp items) over keys, three
-// passes over bricks (one thread = one brick = M consecutive keys, blocks of
+// Exclusive scans of (counts, spread items, interp items, interp m-tiles of 8
+// particles) over keys, three passes over bricks (one thread = one brick = M consecutive keys, blocks of
 // kSchedT bricks): per-block totals, one-CTA scan of the block totals, per-block
 // scan + writes.  offsets[k] / ioff[k]: first particle / interp item of key k;
 // soff[brick key]: first spread item of the brick (soff[k], k not a brick's first
-// key: end of its brick's items); [nkeys] = totals.
+// key: end of its brick's items); moff[k]: interpolation cost before key k, in
+// m-tiles of 8 particles plus kBrickCost per non-empty brick (the persistent
+// interpolation kernel balances its CTAs' item runs by it); [nkeys] = totals.
 constexpr int kSchedT = 256;
+constexpr int kQ = 4;  // scanned quantities
+// Cost of a non-empty brick's slab loads in the interpolation kernel, in m-tiles
+// (sparse regions: one m-tile per brick would otherwise look free)
+#ifndef PIF_SLAB_BRICK_COST
+#define PIF_SLAB_BRICK_COST 12
+#endif
+constexpr int kBrickCost = PIF_SLAB_BRICK_COST;
 
 __device__ __forceinline__ void brick_sums(const int* __restrict__ counts, int64_t i0, int M,
-                                           int a[3]) {
-  int bs = 0, it = 0;
+                                           int a[kQ]) {
+  int bs = 0, it = 0, mt = 0;
   for (int m = 0; m < M; ++m) {
     const int c = counts[i0 + m];
     bs += c;
     it += (c + kInterpItem - 1) / kInterpItem;
+    mt += (c + 7) >> 3;
   }
   a[0] = bs;
   a[1] = (bs + kSpreadItem - 1) / kSpreadItem;
   a[2] = it;
+  a[3] = mt + (bs > 0 ? kBrickCost : 0);
 }
 
-// Block-wide exclusive scan of three ints (blockDim.x == kSchedT); returns the
+// Block-wide exclusive scan of kQ ints (blockDim.x == kSchedT); returns the
 // block totals in tot.
-__device__ __forceinline__ void block_scan3(const int a[3], int ex[3], int tot[3]) {
-  __shared__ int sh[3][kSchedT / 32];
+__device__ __forceinline__ void block_scan(const int a[kQ], int ex[kQ], int tot[kQ]) {
+  __shared__ int sh[kQ][kSchedT / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int incl[3];
+  int incl[kQ];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < kQ; ++q) {
     int v = a[q];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -73,7 +84,7 @@ __device__ __forceinline__ void block_scan3(const int a[3], int ex[3], int tot[3
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < kQ; ++q) {
     int before = 0, all = 0;
 #pragma unroll
     for (int w = 0; w < kSchedT / 32; ++w) {
@@ -89,24 +100,24 @@ __device__ __forceinline__ void block_scan3(const int a[3], int ex[3], int tot[3
 __global__ void __launch_bounds__(kSchedT) k_sched_reduce(const int* __restrict__ counts, Sched S,
                                                           int M) {
   const int64_t nb = S.nkeys / M, br = blockIdx.x * (int64_t)kSchedT + threadIdx.x;
-  int a[3] = {0, 0, 0}, ex[3], tot[3];
+  int a[kQ] = {0, 0, 0, 0}, ex[kQ], tot[kQ];
   if (br < nb) brick_sums(counts, br * M, M, a);
-  block_scan3(a, ex, tot);
+  block_scan(a, ex, tot);
   if (threadIdx.x == 0)
-    for (int q = 0; q < 3; ++q) S.part[3 * blockIdx.x + q] = tot[q];
+    for (int q = 0; q < kQ; ++q) S.part[kQ * blockIdx.x + q] = tot[q];
 }
 
-// In place: part[3 b + q] <- sum of part[3 b' + q] over b' < b (one CTA).
+// In place: part[kQ b + q] <- sum of part[kQ b' + q] over b' < b (one CTA).
 __global__ void __launch_bounds__(1024) k_sched_partials(Sched S, int nblk) {
-  __shared__ int sh[3][32];
+  __shared__ int sh[kQ][32];
   const int T = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int per = (nblk + T - 1) / T, lo = min(nblk, t * per), hi = min(nblk, lo + per);
-  int a[3] = {0, 0, 0};
+  int a[kQ] = {0, 0, 0, 0};
   for (int i = lo; i < hi; ++i)
-    for (int q = 0; q < 3; ++q) a[q] += S.part[3 * i + q];
-  int incl[3];
+    for (int q = 0; q < kQ; ++q) a[q] += S.part[kQ * i + q];
+  int incl[kQ];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < kQ; ++q) {
     int v = a[q];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -119,7 +130,7 @@ __global__ void __launch_bounds__(1024) k_sched_partials(Sched S, int nblk) {
   __syncthreads();
   if (wid == 0) {
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < kQ; ++q) {
       int w = lane < (T >> 5) ? sh[q][lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -130,13 +141,13 @@ __global__ void __launch_bounds__(1024) k_sched_partials(Sched S, int nblk) {
     }
   }
   __syncthreads();
-  int ex[3];
+  int ex[kQ];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) ex[q] = incl[q] - a[q] + (wid > 0 ? sh[q][wid - 1] : 0);
+  for (int q = 0; q < kQ; ++q) ex[q] = incl[q] - a[q] + (wid > 0 ? sh[q][wid - 1] : 0);
   for (int i = lo; i < hi; ++i)
-    for (int q = 0; q < 3; ++q) {
-      const int x = S.part[3 * i + q];
-      S.part[3 * i + q] = ex[q];
+    for (int q = 0; q < kQ; ++q) {
+      const int x = S.part[kQ * i + q];
+      S.part[kQ * i + q] = ex[q];
       ex[q] += x;
     }
 }
@@ -144,27 +155,31 @@ __global__ void __launch_bounds__(1024) k_sched_partials(Sched S, int nblk) {
 __global__ void __launch_bounds__(kSchedT) k_sched_apply(const int* __restrict__ counts, Sched S,
                                                          int M) {
   const int64_t nk = S.nkeys, nb = nk / M, br = blockIdx.x * (int64_t)kSchedT + threadIdx.x;
-  int a[3] = {0, 0, 0}, ex[3], tot[3];
+  int a[kQ] = {0, 0, 0, 0}, ex[kQ], tot[kQ];
   if (br < nb) brick_sums(counts, br * M, M, a);
-  block_scan3(a, ex, tot);
+  block_scan(a, ex, tot);
   if (br >= nb) return;
 #pragma unroll
-  for (int q = 0; q < 3; ++q) ex[q] += S.part[3 * blockIdx.x + q];
+  for (int q = 0; q < kQ; ++q) ex[q] += S.part[kQ * blockIdx.x + q];
   const int64_t i = br * M;
   S.soff[i] = ex[1];
   ex[1] += a[1];
+  if (a[0] > 0) ex[3] += kBrickCost;  // before the brick's first item
   for (int m = 0; m < M; ++m) {
     const int c = counts[i + m];
     S.offsets[i + m] = ex[0];
     S.ioff[i + m] = ex[2];
+    S.moff[i + m] = ex[3];
     if (m) S.soff[i + m] = ex[1];
     ex[0] += c;
     ex[2] += (c + kInterpItem - 1) / kInterpItem;
+    ex[3] += (c + 7) >> 3;
   }
   if (br == nb - 1) {
     S.offsets[nk] = ex[0];
     S.soff[nk] = ex[1];
     S.ioff[nk] = ex[2];
+    S.moff[nk] = ex[3];
   }
 }
 
@@ -175,7 +190,9 @@ __global__ void k_schedule_fill(Sched S, int M) {
   if (k >= S.nkeys) return;
   const int a = S.offsets[k], b = S.offsets[k + 1];
   int it = S.ioff[k];
-  for (int s0 = a; s0 < b; s0 += kInterpItem) S.iitems[it++] = make_int4((int)k, s0, min(b, s0 + kInterpItem), 0);
+  // .w = the item's first m-tile in the concatenated m-tile sequence (key order)
+  for (int s0 = a; s0 < b; s0 += kInterpItem)
+    S.iitems[it++] = make_int4((int)k, s0, min(b, s0 + kInterpItem), S.moff[k] + ((s0 - a) >> 3));
   if (k % M == 0) {
     const int e = S.offsets[k + M];
     int si = S.soff[k];

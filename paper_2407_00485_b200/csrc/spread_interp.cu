@@ -455,6 +455,9 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
         gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
         gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
         const double* src = grid3 + ((int64_t)gx * n + gy) * n;
+#ifdef PIF_EXP_NOLOAD  // timing experiment only: stale tiles after the first NBUF items
+        if (it.k < C::NBUF)
+#endif
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
@@ -548,6 +551,9 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
     prefetch(buf ^ 1, q + C::NW);  // xv[buf ^ 1] was released by the previous m-tile
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
+#ifdef PIF_EXP_NOSTAGE  // timing experiment only: stale psi rows after the first m-tile
+    if (q == wid)
+#endif
     stage(buf, cnt);
     const int tb = c.k % C::NBUF;
     mbar_wait(&S.full[tb], (c.k / C::NBUF) & 1);  // g tile of this item landed
@@ -590,7 +596,11 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
       e1 += __shfl_xor_sync(0xffffffffu, e1, o);
       e2 += __shfl_xor_sync(0xffffffffu, e2, o);
     }
+#ifdef PIF_EXP_NOPUSH  // timing experiment only: no push / stores
+    if (tq == 0 && gr < cnt && e0 == 1.2345e300) {
+#else
     if (tq == 0 && gr < cnt) {
+#endif
       const int64_t j = b + gr;
       if (Eout) {
         const int64_t k = id[j];
@@ -611,6 +621,335 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
       }
     }
     __syncwarp();  // psi rows and xv[buf] are rewritten for the next m-tile
+  }
+  cp_async_wait_all();
+}
+
+// ------------------------------------------------ interp+push, slab ring --
+// The same contraction as k_interp_push, but the g tile of an item is read from
+// a ring of z-slabs of its BRICK (the spreading brick: BX x BY columns, SBZ z
+// rows = one sub-brick height, 3 components) instead of a private copy per item.
+// Each CTA takes a contiguous run of items in key order (brick-major, bz fastest,
+// balanced by m-tile count, Sched::moff), so the items of one brick share its
+// RZ / SBZ slabs and the next brick along z needs only one new slab: the producer warp
+// loads 1/4 of a tile per brick step (w = 13) and runs up to NS - RZ / SBZ slabs
+// ahead of the consumers, with the smem of ~1.8 tiles instead of 2.
+//
+// Virtual slab numbers: item k of the CTA uses slabs V_k .. V_k + NSZ - 1 (ring
+// slot = v % NS), V_0 = 0; the next item of the same brick keeps V, the next
+// brick of the same (bx, by) column at bz' > bz shifts V by min(bz' - bz, NSZ),
+// anything else by NSZ (all slabs new).  Protocol: full[k % ND] -- the
+// producer's cp.async of every slab item k needs have landed; done[k % ND] --
+// every consumer warp has passed item k.  The producer overwrites a slot only
+// after done[] of the last item that used it, and never runs more than ND items
+// ahead (done[k - ND]), so the parity waits never alias.
+//
+// Slab layout: [cy * CS + cx][d][r] (r < SBZ rows), CS = 18 for BX = 16: the
+// B-fragment reads (lane (g, t): tile row 8 nt + g, sub-window column 4 ks + t)
+// are conflict-free for every sub-brick offset (checked exhaustively).
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ>
+struct SlabCfg {
+  using I = InterpCfg<RX, RY, RZ>;
+  static constexpr int KS = I::KS, NT = I::NT;
+  static constexpr int SX = I::SX, SY = I::SY, SZ = I::SZ, OY = I::OY, OZ = I::OZ, WP = I::WP;
+  static constexpr int CS = BX + 2;                 // columns per brick row (2 pad)
+  static constexpr int SLAB = BY * CS * 3 * SBZ;    // doubles per slab
+  static constexpr int NSZ = RZ / SBZ;              // slabs per tile
+  static constexpr int ND = 16;                     // full / done barrier ring
+#ifndef PIF_SLAB_NS
+#define PIF_SLAB_NS 5
+#endif
+  static constexpr int NS = PIF_SLAB_NS;            // slab ring
+#ifndef PIF_SLAB_NW
+#define PIF_SLAB_NW 16
+#endif
+  static constexpr int BYTES = 232448 - 2 * ND * 8 - 64;
+  static constexpr int NWFIT = (BYTES / 8 - NS * SLAB) / (WP + 96);
+  static constexpr int NW = NWFIT < PIF_SLAB_NW ? NWFIT : PIF_SLAB_NW;
+  static_assert(RZ % SBZ == 0 && RZ % 8 == 0 && 8 % SBZ == 0 || SBZ % 8 == 0, "slab rows");
+  static_assert(NS > NSZ, "slab ring must hold a tile plus lookahead");
+  static_assert(NW >= 8, "slab ring too large");
+};
+
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ>
+struct SlabSmem {
+  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ>;
+  double slab[C::NS][C::SLAB];
+  double psi[C::NW][C::WP];
+  double xv[C::NW][2][6][8];
+  unsigned long long full[C::ND], done[C::ND];
+  int range[2];
+};
+
+// Item k of this CTA's run (global index lo + k): particle range, tile origin,
+// sub-brick column offset and virtual slab number (needs the previous item's
+// brick coordinates: call in order of k).
+struct SlabCursor {
+  int k, base, m;
+  int64_t start, end;
+  int T0[3];
+  int ox, oy, V;
+  int bcol, bz;  // brick column (bx * NB1 + by) and bz of item k
+};
+
+template <int NSZ>
+__device__ __forceinline__ void slab_cursor_load(SlabCursor& it, int lo, const Brick& g,
+                                                 const Sched& Sc) {
+  const int4 e = Sc.iitems[lo + it.k];
+  it.start = e.y;
+  it.end = e.z;
+  it.m = (int)((e.z - e.y + 7) >> 3);
+  const int M = g.m[0] * g.m[1] * g.m[2];
+  const int brick = e.x / M, sk = e.x % M;
+  const int bz = brick % g.NB[2], bcol = brick / g.NB[2];
+  const int by = bcol % g.NB[1], bx = bcol / g.NB[1];
+  const int sy = (sk / g.m[2]) % g.m[1], sx = sk / (g.m[2] * g.m[1]);
+  it.ox = sx * g.ib[0];
+  it.oy = sy * g.ib[1];
+  it.T0[0] = bx * g.sb[0] - g.hw + it.ox;
+  it.T0[1] = by * g.sb[1] - g.hw + it.oy;
+  it.T0[2] = bz * g.sb[2] - g.hw;
+  if (it.k == 0) it.V = 0;
+  else if (bcol == it.bcol && bz == it.bz) {
+  } else if (bcol == it.bcol && bz > it.bz) it.V += min(bz - it.bz, NSZ);
+  else it.V += NSZ;
+  it.bcol = bcol;
+  it.bz = bz;
+}
+
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ>
+__global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ>::NW + 1), 1)
+    k_interp_push_slab(const double* __restrict__ grid3, double* __restrict__ x,
+                       double* __restrict__ v, int64_t stride, const int* __restrict__ id,
+                       double* __restrict__ Eout, const Sched Sc, Brick g,
+                       const __grid_constant__ Horner hc, PushArgs P) {
+  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SlabSmem<RX, RY, RZ, BX, BY, SBZ>& S = *reinterpret_cast<SlabSmem<RX, RY, RZ, BX, BY, SBZ>*>(smem_raw);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int n = g.n;
+  const int64_t n3 = (int64_t)n * n * n;
+  if (threadIdx.x == 0) {
+    // contiguous item run of this CTA: items whose first m-tile lies in
+    // [b M / G, (b + 1) M / G), M = all m-tiles (iitems[].w, increasing)
+    const int total = Sc.ioff[Sc.nkeys];
+    const int64_t Mt = Sc.moff[Sc.nkeys];
+    int r[2];
+    for (int q = 0; q < 2; ++q) {
+      const int64_t target = (int64_t)(blockIdx.x + q) * Mt / gridDim.x;
+      int a = 0, b = total;  // first item with first m-tile >= target
+      while (a < b) {
+        const int mid = (a + b) >> 1;
+        if ((int64_t)Sc.iitems[mid].w < target) a = mid + 1;
+        else b = mid;
+      }
+      r[q] = (blockIdx.x + q == gridDim.x) ? total : a;
+    }
+    S.range[0] = r[0];
+    S.range[1] = r[1];
+    for (int b = 0; b < C::ND; ++b) {
+      mbar_init(&S.full[b], 32);
+      mbar_init(&S.done[b], C::NW);
+    }
+  }
+  __syncthreads();
+  const int lo = S.range[0], nitems = S.range[1] - S.range[0];
+  if (nitems <= 0) return;
+
+  if (wid == C::NW) {
+    // ---- producer: the new slabs of item k -> ring slots, then full[k].
+    // Lane = (column j of 8, row r of 4): a 32-byte z run of one (column, d).
+    constexpr int RQ = SBZ < 4 ? SBZ : 4;   // rows per instruction
+    constexpr int CQ = 32 / RQ;             // columns per instruction
+    const int r0 = lane % RQ, j0 = lane / RQ;
+    int lastuse[C::NS];
+#pragma unroll
+    for (int s2 = 0; s2 < C::NS; ++s2) lastuse[s2] = -1;
+    int loaded = 0;
+    SlabCursor it;
+    it.V = 0;
+    it.bcol = it.bz = -1;
+    for (it.k = 0; it.k < nitems; ++it.k) {
+      slab_cursor_load<C::NSZ>(it, lo, g, Sc);
+      if (it.k >= C::ND) mbar_wait(&S.done[(it.k - C::ND) % C::ND], ((it.k - C::ND) / C::ND) & 1);
+      for (int vs = max(loaded, it.V); vs < it.V + C::NSZ; ++vs) {
+        const int slot = vs % C::NS;
+        int j = -1;
+#pragma unroll
+        for (int s2 = 0; s2 < C::NS; ++s2)
+          if (s2 == slot) j = lastuse[s2];
+        if (j >= 0 && j > it.k - C::ND) mbar_wait(&S.done[j % C::ND], (j / C::ND) & 1);
+        const int i = vs - it.V;  // slab of the tile: rows T0z + i SBZ ..
+        double* dst = S.slab[slot];
+        const int Bx0 = it.T0[0] - it.ox, By0 = it.T0[1] - it.oy;
+        for (int rq = 0; rq < SBZ; rq += RQ) {
+          const int r = rq + r0;
+          int gz = it.T0[2] + i * SBZ + r;
+          gz = gz < 0 ? gz + n : (gz >= n ? gz - n : gz);
+          for (int c0 = 0; c0 < BX * BY; c0 += CQ) {
+            const int cc = c0 + j0;
+            if (cc < BX * BY) {
+              const int cy = cc / BX, cx = cc - cy * BX;
+              int gx = Bx0 + cx, gy = By0 + cy;
+              gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
+              gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
+              const double* src = grid3 + ((int64_t)gx * n + gy) * n + gz;
+              double* d0 = dst + ((cy * C::CS + cx) * 3) * SBZ + r;
+#pragma unroll
+              for (int d = 0; d < 3; ++d) cp_async8(d0 + d * SBZ, src + d * n3);
+            }
+          }
+        }
+      }
+      loaded = max(loaded, it.V + C::NSZ);
+#pragma unroll
+      for (int s2 = 0; s2 < C::NS; ++s2) {
+        const int off = (s2 - it.V % C::NS + C::NS) % C::NS;  // slot s2 = (V + off) % NS
+        if (off < C::NSZ) lastuse[s2] = it.k;
+      }
+      cp_async_mbar_arrive(&S.full[it.k % C::ND]);
+    }
+    cp_async_wait_all();
+    return;
+  }
+
+  // ---- consumers (as k_interp_push; B fragments from the slab ring)
+  const int gr = lane >> 2, tq = lane & 3;
+  double* const wpsi = S.psi[wid];
+  double (*const xv)[6][8] = S.xv[wid];
+  const double two_over_w = 2.0 / g.w;
+  const double flo = g.odd ? -0.5 : 0.0;
+  SlabCursor c, pf;
+  c.k = pf.k = 0;
+  c.base = pf.base = 0;
+  c.V = 0;
+  c.bcol = c.bz = -1;
+  slab_cursor_load<C::NSZ>(c, lo, g, Sc);
+  pf = c;
+  auto advance = [&](SlabCursor& it, int q, bool release) {
+    while (it.k < nitems && q >= it.base + it.m) {
+      if (release) {
+        mbar_wait(&S.full[it.k % C::ND], (it.k / C::ND) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.done[it.k % C::ND]);
+      }
+      it.base += it.m;
+      if (++it.k < nitems) slab_cursor_load<C::NSZ>(it, lo, g, Sc);
+    }
+    return it.k < nitems;
+  };
+  auto prefetch = [&](int buf, int q) {
+    if (advance(pf, q, false)) {
+      const int64_t b = pf.start + 8 * (int64_t)(q - pf.base);
+      const int cnt = (int)min((int64_t)8, pf.end - b);
+      for (int u = lane; u < 48; u += 32) {
+        const int comp = u >> 3, p = u & 7;
+        if (p < cnt) {
+          if (comp < 3) cp_async8(&xv[buf][comp][p], x + comp * stride + b + p);
+          else if (v) cp_async8(&xv[buf][comp][p], v + (comp - 3) * stride + b + p);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  auto stage = [&](int buf, int cnt) {
+    if (lane < 24) {
+      const int p = lane & 7, d = lane >> 3;
+      const int R = d == 0 ? RX : (d == 1 ? RY : InterpCfg<RX, RY, RZ>::ZP);
+      double* row = wpsi + (d == 0 ? p * C::SX : (d == 1 ? C::OY + p * C::SY : C::OZ + p * C::SZ));
+      constexpr int ZP = InterpCfg<RX, RY, RZ>::ZP;
+#pragma unroll
+      for (int u = 0; u < (RX > ZP ? RX : (RY > ZP ? RY : ZP)); ++u)
+        if (u < R) row[u] = 0.0;
+      if (p < cnt) {
+        const int T0d = d == 0 ? c.T0[0] : (d == 1 ? c.T0[1] : c.T0[2]);
+        double xs = xv[buf][d][p] * g.scale;
+        const int a = anchor_of(xs, g);
+        const double f = xs - (double)a;
+        double* wrow = row + (a - g.hw - T0d);
+        const double sv = 2.0 * (f - flo) - 1.0;
+        psi_row(wrow, 0, f, sv, hc, g, two_over_w);
+      }
+    }
+  };
+
+  int buf = 0;
+  prefetch(0, wid);
+  for (int q = wid; advance(c, q, true); q += C::NW, buf ^= 1) {
+    const int64_t b = c.start + 8 * (int64_t)(q - c.base);
+    const int cnt = (int)min((int64_t)8, c.end - b);
+    prefetch(buf ^ 1, q + C::NW);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    stage(buf, cnt);
+    mbar_wait(&S.full[c.k % C::ND], (c.k / C::ND) & 1);  // every slab of this item landed
+    __syncwarp();
+    // this lane's B-fragment rows: tile row zl = 8 nt + gr -> slab zl / SBZ, row zl % SBZ
+    const double* Pb[C::NT];
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) {
+      const int zl = 8 * nt + gr;
+      Pb[nt] = &S.slab[(c.V + zl / SBZ) % C::NS][0] + (zl % SBZ) +
+               (c.oy * C::CS + c.ox) * 3 * SBZ;
+    }
+    double acc[C::NT][3][2];
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) acc[nt][d][0] = acc[nt][d][1] = 0.0;
+    const double* pxr = wpsi + gr * C::SX;
+    const double* pyr = wpsi + C::OY + gr * C::SY;
+    int cx = tq % RX, cy = tq / RX;
+#pragma unroll 2
+    for (int ks = 0; ks < C::KS; ++ks) {
+      const double a = pxr[cx] * pyr[cy];
+      const int off = (cy * C::CS + cx) * 3 * SBZ;
+      cx += 4;
+      if (cx >= RX) {
+        cx -= RX;
+        cy += 1;
+      }
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, Pb[nt][off + d * SBZ]);
+    }
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    const double* pzr = wpsi + C::OZ + gr * C::SZ;
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) {
+      const double2 wz = *reinterpret_cast<const double2*>(pzr + 8 * nt + 2 * tq);
+      e0 = fma(wz.x, acc[nt][0][0], fma(wz.y, acc[nt][0][1], e0));
+      e1 = fma(wz.x, acc[nt][1][0], fma(wz.y, acc[nt][1][1], e1));
+      e2 = fma(wz.x, acc[nt][2][0], fma(wz.y, acc[nt][2][1], e2));
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      e0 += __shfl_xor_sync(0xffffffffu, e0, o);
+      e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+      e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    }
+    if (tq == 0 && gr < cnt) {
+      const int64_t j = b + gr;
+      if (Eout) {
+        const int64_t k = id[j];
+        Eout[k] = e0;
+        Eout[stride + k] = e1;
+        Eout[2 * stride + k] = e2;
+      }
+      if (P.kicks > 0 || P.drift) {
+        double x0 = xv[buf][0][gr], x1 = xv[buf][1][gr], x2 = xv[buf][2][gr];
+        double v0 = xv[buf][3][gr], v1 = xv[buf][4][gr], v2 = xv[buf][5][gr];
+        push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
+        x[j] = x0;
+        x[stride + j] = x1;
+        x[2 * stride + j] = x2;
+        v[j] = v0;
+        v[stride + j] = v1;
+        v[2 * stride + j] = v2;
+      }
+    }
+    __syncwarp();
   }
   cp_async_wait_all();
 }
@@ -679,10 +1018,45 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
   return cudaGetLastError();
 }
 
+template <int A, int B, int Cz, int BX, int BY, int SBZ>
+static cudaError_t interp_slab_launch(unsigned nsub, const double* grid3, double* x, double* v,
+                                      int64_t stride, const int* id, double* Eout,
+                                      const Sched& offsets, const Brick& g, const Horner& hc,
+                                      const PushArgs& P, cudaStream_t st) {
+  using C = SlabCfg<A, B, Cz, BX, BY, SBZ>;
+  const int T = 32 * (C::NW + 1);
+  const size_t smem = sizeof(SlabSmem<A, B, Cz, BX, BY, SBZ>);
+  static int sms = 0;
+  if (!sms) {
+    cudaError_t e = cudaFuncSetAttribute(k_interp_push_slab<A, B, Cz, BX, BY, SBZ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, per = 0;
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push_slab<A, B, Cz, BX, BY, SBZ>,
+                                                        T, smem);
+    if (e != cudaSuccess) return e;
+    if (per < 1) return cudaErrorInvalidConfiguration;
+  }
+  // persistent: one CTA per SM, each with a contiguous run of items
+  const unsigned grid = nsub < (unsigned)sms ? nsub : (unsigned)sms;
+  if (grid == 0) return cudaSuccess;
+  k_interp_push_slab<A, B, Cz, BX, BY, SBZ><<<grid, T, smem, st>>>(grid3, x, v, stride, id, Eout,
+                                                                   offsets, g, hc, P);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
                                const int* id, double* Eout, const Sched& offsets, const Brick& g,
                                const Horner& hc, const PushArgs& P, cudaStream_t st) {
   const unsigned nsub = (unsigned)offsets.max_i;  // upper bound on interp items
+#ifndef PIF_NO_SLAB
+  if (g.RI[0] == 14 && g.RI[1] == 14 && g.RI[2] == 16 && g.RS[0] == 16 && g.RS[1] == 16 &&
+      g.ib[2] == 4 && g.m[2] == 1)
+    return interp_slab_launch<14, 14, 16, 16, 16, 4>(nsub, grid3, x, v, stride, id, Eout, offsets,
+                                                     g, hc, P, st);
+#endif
 #define PIF_INTERP(A, B, Cz)                                                                   \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
