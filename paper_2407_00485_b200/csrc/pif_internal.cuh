@@ -81,7 +81,11 @@ __device__ __forceinline__ double es_kernel(double t, double two_over_w, double 
   return r > 0.0 ? exp(beta * (sqrt(r) - 1.0)) : (r == 0.0 ? exp(-beta) : 0.0);
 }
 
+// x - L floor(x / L), L itself mapped to 0.  For 0 <= x < L, x / L rounds to at
+// most 1 - 2^-53 (x <= L - ulp(L)), so floor(x / L) = 0 and the result is x:
+// the division (a ~10-instruction FP64 sequence) runs only for crossing particles.
 __device__ __forceinline__ double wrapL(double x, double L) {
+  if (x >= 0.0 && x < L) return x;
   double y = x - L * floor(x / L);
   return y >= L ? 0.0 : y;
 }
