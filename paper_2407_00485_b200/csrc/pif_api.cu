@@ -248,7 +248,7 @@ size_t layout(pif_ctx c, char* base) {
   for (int i = 0; i < 2; ++i) {
     const Plan& p = c->plan[i];
     if (!p.valid || p.kind != PIF_PROP_PIF_NUFFT) continue;
-    const int64_t M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
+    const int64_t M = keys_per_brick(p.g);
     c->max_s = std::max(c->max_s, sched_max_s(p.nbricks, M, n));
     c->max_i = std::max(c->max_i, sched_max_i(p.nbricks, n));
   }
@@ -335,6 +335,20 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
       g.NB[d] = (n + g.sb[d] - 1) / g.sb[d];
       g.nkeys *= (int64_t)g.NB[d] * m[d];
     }
+    // slab interpolation tiles: keys down to the xy-cells of a sub-brick, so an
+    // m-tile of 8 consecutive particles usually shares one cell and its window
+    // (w = 13: 13 x 13 columns instead of the tile's 14 x 14)
+#ifndef PIF_CELL_KEYS
+#ifdef PIF_NO_SLAB
+#define PIF_CELL_KEYS 0
+#else
+#define PIF_CELL_KEYS 1
+#endif
+#endif
+    const bool slab = (RI[0] == 14 && RI[1] == 14 && RI[2] == 16) || (RI[0] == 10 && RI[1] == 10 && RI[2] == 8) ||
+                      (RI[0] == 6 && RI[1] == 6 && RI[2] == 8);
+    g.C = (PIF_CELL_KEYS && slab && m[2] == 1) ? g.ib[0] * g.ib[1] : 1;
+    g.nkeys *= g.C;
     g.scale = n / L;
     g.beta = es_beta(w);
     horner_fit(w, g.beta, p.hc);
@@ -441,7 +455,7 @@ pif_status ph_mark(pif_ctx c, int ph) {
   } while (0)
 
 Sched sched_of(pif_ctx c, const Plan& p) {
-  const int64_t M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
+  const int64_t M = keys_per_brick(p.g);
   return Sched{c->offsets, c->soff, c->ioff, c->moff, c->sitems, c->iitems, c->spart, p.nbricks,
                sched_max_s(p.nbricks, M, c->nloc), sched_max_i(p.nbricks, c->nloc)};
 }
@@ -451,7 +465,7 @@ pif_status sort_particles(pif_ctx c, Plan& p) {
   const int64_t n = c->nloc;
   CU(cudaMemsetAsync(c->counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(c->xA, n, n, p.g, c->key, c->rnk, c->counts, c->st));
-  CU(launch_schedule(c->counts, sched_of(c, p), p.g.m[0] * p.g.m[1] * p.g.m[2], c->st));
+  CU(launch_schedule(c->counts, sched_of(c, p), keys_per_brick(p.g), p.g.C, c->st));
   CU(launch_scatter_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->xB,
                            c->vB, c->idB, nullptr, c->st));
   std::swap(c->xA, c->xB);
@@ -1185,7 +1199,7 @@ pif_status pif_finalize(pif_ctx c) {
 // ------------------------------------------------------------- debug/tests --
 // Temporary schedule for the debug transforms (one cudaMalloc: counts + Sched).
 static pif_status debug_sched(pif_ctx c, const Plan& p, int64_t n, int** counts, Sched& S) {
-  const int64_t K = p.nbricks, M = (int64_t)p.g.m[0] * p.g.m[1] * p.g.m[2];
+  const int64_t K = p.nbricks, M = keys_per_brick(p.g);
   const int64_t ms = sched_max_s(K, M, n), mi = sched_max_i(K, n);
   const size_t ints = K + 4 * (K + 1) + 4 * ((size_t)K / 256 + 2);
   char* buf = nullptr;
@@ -1225,7 +1239,7 @@ pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, con
   CU(launch_iota(id, n, c->st));
   CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_schedule(counts, S, p.g.m[0] * p.g.m[1] * p.g.m[2], c->st));
+  CU(launch_schedule(counts, S, keys_per_brick(p.g), p.g.C, c->st));
   CU(launch_scatter_sorted(dx, nullptr, id, ds, n, n, key, rk, offs, dx2, nullptr, id2, ds2, c->st));
   CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
   CU(launch_spread(dx2, n, ds2, 1.0, S, p.g, p.hc, p.grid, c->st));
@@ -1264,7 +1278,7 @@ pif_status pif_debug_type2(pif_ctx c, int which, const double* cin, const double
   CU(launch_iota(id, n, c->st));
   CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_schedule(counts, S, p.g.m[0] * p.g.m[1] * p.g.m[2], c->st));
+  CU(launch_schedule(counts, S, keys_per_brick(p.g), p.g.C, c->st));
   CU(launch_scatter_sorted(dx, nullptr, id, nullptr, n, n, key, rk, offs, dx2, nullptr, id2, nullptr, c->st));
   CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, c->st));
   CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3));

@@ -28,7 +28,7 @@ struct Phys {
 // particle's window is the w grid points [a - hw, a - hw + w) around its anchor
 // a (round(x~) for odd w, floor(x~) for even w), hw = (w - 1) / 2, so that
 // |g - x~| <= w / 2 on the whole window.  Sort key (brick-major):
-// key = brick * (m0 m1 m2) + sub-brick-in-brick.
+// key = (brick * (m0 m1 m2) + sub-brick-in-brick) * C + xy-cell-in-sub-brick.
 struct Brick {
   int n;         // upsampled grid points per dimension
   int w;         // kernel width (grid points)
@@ -38,6 +38,7 @@ struct Brick {
   int m[3];      // sub-bricks per spreading brick
   int sb[3];     // cells per spreading brick
   int NB[3];     // spreading bricks per dimension = ceil(n / sb)
+  int C;         // sort keys per sub-brick: 1, or ib0 ib1 (its xy-cells; slab interp)
   int RI[3];     // interpolation tile points
   int RS[3];     // spreading tile points
   int64_t nkeys; // number of sub-bricks = NB0 NB1 NB2 m0 m1 m2
@@ -167,7 +168,9 @@ inline int64_t sched_max_i(int64_t nkeys, int64_t n) { return nkeys + n / kInter
 // All launchers enqueue on `st` and return cudaGetLastError().
 cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const Brick& g, int* key,
                              int* rank, int* counts, cudaStream_t st);
-cudaError_t launch_schedule(const int* counts, const Sched& S, int M, cudaStream_t st);
+cudaError_t launch_schedule(const int* counts, const Sched& S, int M, int C, cudaStream_t st);
+// keys per spreading brick
+inline int keys_per_brick(const Brick& g) { return g.m[0] * g.m[1] * g.m[2] * g.C; }
 cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,
                                   int64_t stride, int64_t n, const int* key, const int* rank,
                                   const int* offsets, double* x2, double* v2, int* id2, double* s2,

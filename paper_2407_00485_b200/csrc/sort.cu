@@ -10,16 +10,20 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
                             int* __restrict__ counts) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
-  int B[3], S[3];
+  int B[3], S[3], Q[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     double xs = x[d * stride + j] * g.scale;
     int a = anchor_of(xs, g);
     B[d] = a / g.sb[d];
-    S[d] = (a - B[d] * g.sb[d]) / g.ib[d];
+    const int r = a - B[d] * g.sb[d];
+    S[d] = r / g.ib[d];
+    Q[d] = r - S[d] * g.ib[d];
   }
   int k = ((B[0] * g.NB[1] + B[1]) * g.NB[2] + B[2]) * (g.m[0] * g.m[1] * g.m[2]) +
           (S[0] * g.m[1] + S[1]) * g.m[2] + S[2];
+  // C > 1: xy-cell of the sub-brick, snake order (consecutive cells adjacent)
+  if (g.C > 1) k = k * g.C + Q[0] * g.ib[1] + ((Q[0] & 1) ? g.ib[1] - 1 - Q[1] : Q[1]);
   key[j] = k;
   // warp-aggregated rank: one atomic per distinct key in the warp (sorted-ish
   // input and crowded bricks give many equal keys per warp)
@@ -33,14 +37,17 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
   rank[j] = base + __popc(peers & ((1u << lane) - 1u));
 }
 
-// Exclusive scans of (counts, spread items, interp items, interp m-tiles of 8
-// particles) over keys, three passes over bricks (one thread = one brick = M consecutive keys, blocks of
-// kSchedT bricks): per-block totals, one-CTA scan of the block totals, per-block
-// scan + writes.  offsets[k] / ioff[k]: first particle / interp item of key k;
-// soff[brick key]: first spread item of the brick (soff[k], k not a brick's first
-// key: end of its brick's items); moff[k]: interpolation cost before key k, in
-// m-tiles of 8 particles plus kBrickCost per non-empty brick (the persistent
-// interpolation kernel balances its CTAs' item runs by it); [nkeys] = totals.
+// Exclusive scans of (counts, spread items, interp items, interpolation cost)
+// over keys, three passes over bricks (one thread = one brick = M consecutive
+// keys, blocks of kSchedT bricks): per-block totals, one-CTA scan of the block
+// totals, per-block scan + writes.  Interp items cover groups of C consecutive
+// keys (one sub-brick; C > 1 when keys are its xy-cells).  offsets[k]: first
+// particle of key k; ioff[k] (k a group's first key): first interp item of the
+// group; soff[k] (k a brick's first key): first spread item of the brick (other
+// keys: the end of their brick's / group's items); moff[k] (group first key):
+// interpolation cost before the group, in m-tiles of 8 particles plus
+// kBrickCost per non-empty brick (the persistent interpolation kernel balances
+// its CTAs' item runs by it); [nkeys] = totals.
 constexpr int kSchedT = 256;
 constexpr int kQ = 4;  // scanned quantities
 // Cost of a non-empty brick's slab loads in the interpolation kernel, in m-tiles
@@ -51,13 +58,14 @@ constexpr int kQ = 4;  // scanned quantities
 constexpr int kBrickCost = PIF_SLAB_BRICK_COST;
 
 __device__ __forceinline__ void brick_sums(const int* __restrict__ counts, int64_t i0, int M,
-                                           int a[kQ]) {
+                                           int C, int a[kQ]) {
   int bs = 0, it = 0, mt = 0;
-  for (int m = 0; m < M; ++m) {
-    const int c = counts[i0 + m];
-    bs += c;
-    it += (c + kInterpItem - 1) / kInterpItem;
-    mt += (c + 7) >> 3;
+  for (int m = 0; m < M; m += C) {
+    int gc = 0;
+    for (int q = 0; q < C; ++q) gc += counts[i0 + m + q];
+    bs += gc;
+    it += (gc + kInterpItem - 1) / kInterpItem;
+    mt += (gc + 7) >> 3;
   }
   a[0] = bs;
   a[1] = (bs + kSpreadItem - 1) / kSpreadItem;
@@ -98,10 +106,10 @@ __device__ __forceinline__ void block_scan(const int a[kQ], int ex[kQ], int tot[
 }
 
 __global__ void __launch_bounds__(kSchedT) k_sched_reduce(const int* __restrict__ counts, Sched S,
-                                                          int M) {
+                                                          int M, int C) {
   const int64_t nb = S.nkeys / M, br = blockIdx.x * (int64_t)kSchedT + threadIdx.x;
   int a[kQ] = {0, 0, 0, 0}, ex[kQ], tot[kQ];
-  if (br < nb) brick_sums(counts, br * M, M, a);
+  if (br < nb) brick_sums(counts, br * M, M, C, a);
   block_scan(a, ex, tot);
   if (threadIdx.x == 0)
     for (int q = 0; q < kQ; ++q) S.part[kQ * blockIdx.x + q] = tot[q];
@@ -153,10 +161,10 @@ __global__ void __launch_bounds__(1024) k_sched_partials(Sched S, int nblk) {
 }
 
 __global__ void __launch_bounds__(kSchedT) k_sched_apply(const int* __restrict__ counts, Sched S,
-                                                         int M) {
+                                                         int M, int C) {
   const int64_t nk = S.nkeys, nb = nk / M, br = blockIdx.x * (int64_t)kSchedT + threadIdx.x;
   int a[kQ] = {0, 0, 0, 0}, ex[kQ], tot[kQ];
-  if (br < nb) brick_sums(counts, br * M, M, a);
+  if (br < nb) brick_sums(counts, br * M, M, C, a);
   block_scan(a, ex, tot);
   if (br >= nb) return;
 #pragma unroll
@@ -165,15 +173,23 @@ __global__ void __launch_bounds__(kSchedT) k_sched_apply(const int* __restrict__
   S.soff[i] = ex[1];
   ex[1] += a[1];
   if (a[0] > 0) ex[3] += kBrickCost;  // before the brick's first item
-  for (int m = 0; m < M; ++m) {
-    const int c = counts[i + m];
-    S.offsets[i + m] = ex[0];
+  for (int m = 0; m < M; m += C) {
+    int gc = 0;
+    for (int q = 0; q < C; ++q) {
+      const int c = counts[i + m + q];
+      S.offsets[i + m + q] = ex[0] + gc;
+      if (m + q) S.soff[i + m + q] = ex[1];
+      gc += c;
+    }
     S.ioff[i + m] = ex[2];
     S.moff[i + m] = ex[3];
-    if (m) S.soff[i + m] = ex[1];
-    ex[0] += c;
-    ex[2] += (c + kInterpItem - 1) / kInterpItem;
-    ex[3] += (c + 7) >> 3;
+    ex[0] += gc;
+    ex[2] += (gc + kInterpItem - 1) / kInterpItem;
+    ex[3] += (gc + 7) >> 3;
+    for (int q = 1; q < C; ++q) {
+      S.ioff[i + m + q] = ex[2];
+      S.moff[i + m + q] = ex[3];
+    }
   }
   if (br == nb - 1) {
     S.offsets[nk] = ex[0];
@@ -183,16 +199,19 @@ __global__ void __launch_bounds__(kSchedT) k_sched_apply(const int* __restrict__
   }
 }
 
-// One thread per key: write the interp items of the key, and (first key of a
-// brick) the spread items of the brick.
-__global__ void k_schedule_fill(Sched S, int M) {
+// One thread per key: (first key of a group) the interp items of the group,
+// and (first key of a brick) the spread items of the brick.
+__global__ void k_schedule_fill(Sched S, int M, int C) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= S.nkeys) return;
-  const int a = S.offsets[k], b = S.offsets[k + 1];
-  int it = S.ioff[k];
-  // .w = the item's first m-tile in the concatenated m-tile sequence (key order)
-  for (int s0 = a; s0 < b; s0 += kInterpItem)
-    S.iitems[it++] = make_int4((int)k, s0, min(b, s0 + kInterpItem), S.moff[k] + ((s0 - a) >> 3));
+  const int a = S.offsets[k];
+  if (k % C == 0) {
+    const int b = S.offsets[k + C];
+    int it = S.ioff[k];
+    // .w = the item's cost offset (m-tiles, key order)
+    for (int s0 = a; s0 < b; s0 += kInterpItem)
+      S.iitems[it++] = make_int4((int)k, s0, min(b, s0 + kInterpItem), S.moff[k] + ((s0 - a) >> 3));
+  }
   if (k % M == 0) {
     const int e = S.offsets[k + M];
     int si = S.soff[k];
@@ -245,12 +264,12 @@ cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const B
   if (n > 0) k_bin_count<<<nblk(n, 256), 256, 0, st>>>(x, stride, n, g, key, rank, counts);
   return cudaGetLastError();
 }
-cudaError_t launch_schedule(const int* counts, const Sched& S, int M, cudaStream_t st) {
+cudaError_t launch_schedule(const int* counts, const Sched& S, int M, int C, cudaStream_t st) {
   const unsigned nsb = nblk_sched(S.nkeys, M);
-  k_sched_reduce<<<nsb, kSchedT, 0, st>>>(counts, S, M);
+  k_sched_reduce<<<nsb, kSchedT, 0, st>>>(counts, S, M, C);
   k_sched_partials<<<1, 1024, 0, st>>>(S, (int)nsb);
-  k_sched_apply<<<nsb, kSchedT, 0, st>>>(counts, S, M);
-  k_schedule_fill<<<nblk(S.nkeys, 256), 256, 0, st>>>(S, M);
+  k_sched_apply<<<nsb, kSchedT, 0, st>>>(counts, S, M, C);
+  k_schedule_fill<<<nblk(S.nkeys, 256), 256, 0, st>>>(S, M, C);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,

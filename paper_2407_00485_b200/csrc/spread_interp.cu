@@ -647,33 +647,44 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
 // Slab layout: [cy * CS + cx][d][r] (r < SBZ rows), CS = 18 for BX = 16: the
 // B-fragment reads (lane (g, t): tile row 8 nt + g, sub-window column 4 ks + t)
 // are conflict-free for every sub-brick offset (checked exhaustively).
-template <int RX, int RY, int RZ, int BX, int BY, int SBZ>
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX>
 struct SlabCfg {
   using I = InterpCfg<RX, RY, RZ>;
   static constexpr int KS = I::KS, NT = I::NT;
   static constexpr int SX = I::SX, SY = I::SY, SZ = I::SZ, OY = I::OY, OZ = I::OZ, WP = I::WP;
-  static constexpr int CS = BX + 2;                 // columns per brick row (2 pad)
-  static constexpr int SLAB = BY * CS * 3 * SBZ;    // doubles per slab
+  static constexpr int CS = CSX;                    // columns per brick row (>= BX)
+  // doubles per slab: BY + 1 rows (the last one zero); one-row slabs (SBZ = 1)
+  // are padded to 4 (mod 16) so that the 4 slabs of a half-warp's fragment rows
+  // fall in different banks (conflict pattern checked exhaustively)
+  static constexpr int SLAB0 = (BY + 1) * CS * 3 * SBZ;
+  static constexpr int SLAB = SBZ == 1 ? SLAB0 + ((20 - SLAB0 % 16) % 16) : SLAB0;
   static constexpr int NSZ = RZ / SBZ;              // slabs per tile
   static constexpr int ND = 16;                     // full / done barrier ring
 #ifndef PIF_SLAB_NS
 #define PIF_SLAB_NS 5
 #endif
-  static constexpr int NS = PIF_SLAB_NS;            // slab ring
+  // slab ring: a tile plus the lookahead (brick steps along z)
+  static constexpr int NS = NSZ == 4 ? PIF_SLAB_NS : (SBZ == 1 ? NSZ + 4 : NSZ + 2);
 #ifndef PIF_SLAB_NW
 #define PIF_SLAB_NW 16
 #endif
   static constexpr int BYTES = 232448 - 2 * ND * 8 - 64;
   static constexpr int NWFIT = (BYTES / 8 - NS * SLAB) / (WP + 96);
   static constexpr int NW = NWFIT < PIF_SLAB_NW ? NWFIT : PIF_SLAB_NW;
-  static_assert(RZ % SBZ == 0 && RZ % 8 == 0 && 8 % SBZ == 0 || SBZ % 8 == 0, "slab rows");
+  // psi rows are zero-filled to FILL entries (px < RX, py <= RY: the padded
+  // columns of a window's last k step, pz < ZP)
+  static constexpr int FILL0 = RX > RY + 1 ? RX : RY + 1;
+  static constexpr int FILL = FILL0 > I::ZP ? FILL0 : I::ZP;
+  static_assert(FILL <= SX && FILL <= SY && FILL <= SZ, "psi row strides");
+  static_assert(CS >= BX, "brick row");
+  static_assert(RZ % SBZ == 0 && RZ % 8 == 0 && (SBZ == 1 || SBZ == 4), "slab rows");
   static_assert(NS > NSZ, "slab ring must hold a tile plus lookahead");
   static_assert(NW >= 8, "slab ring too large");
 };
 
-template <int RX, int RY, int RZ, int BX, int BY, int SBZ>
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX>
 struct SlabSmem {
-  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ>;
+  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>;
   double slab[C::NS][C::SLAB];
   double psi[C::NW][C::WP];
   double xv[C::NW][2][6][8];
@@ -700,7 +711,7 @@ __device__ __forceinline__ void slab_cursor_load(SlabCursor& it, int lo, const B
   it.end = e.z;
   it.m = (int)((e.z - e.y + 7) >> 3);
   const int M = g.m[0] * g.m[1] * g.m[2];
-  const int brick = e.x / M, sk = e.x % M;
+  const int brick = e.x / (M * g.C), sk = (e.x / g.C) % M;  // e.x: the sub-brick's first key
   const int bz = brick % g.NB[2], bcol = brick / g.NB[2];
   const int by = bcol % g.NB[1], bx = bcol / g.NB[1];
   const int sy = (sk / g.m[2]) % g.m[1], sx = sk / (g.m[2] * g.m[1]);
@@ -717,15 +728,15 @@ __device__ __forceinline__ void slab_cursor_load(SlabCursor& it, int lo, const B
   it.bz = bz;
 }
 
-template <int RX, int RY, int RZ, int BX, int BY, int SBZ>
-__global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ>::NW + 1), 1)
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX>
+__global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>::NW + 1), 1)
     k_interp_push_slab(const double* __restrict__ grid3, double* __restrict__ x,
                        double* __restrict__ v, int64_t stride, const int* __restrict__ id,
                        double* __restrict__ Eout, const Sched Sc, Brick g,
                        const __grid_constant__ Horner hc, PushArgs P) {
-  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ>;
+  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SlabSmem<RX, RY, RZ, BX, BY, SBZ>& S = *reinterpret_cast<SlabSmem<RX, RY, RZ, BX, BY, SBZ>*>(smem_raw);
+  SlabSmem<RX, RY, RZ, BX, BY, SBZ, CSX>& S = *reinterpret_cast<SlabSmem<RX, RY, RZ, BX, BY, SBZ, CSX>*>(smem_raw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n = g.n;
   const int64_t n3 = (int64_t)n * n * n;
@@ -751,6 +762,12 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ>::NW + 1
       mbar_init(&S.full[b], 32);
       mbar_init(&S.done[b], C::NW);
     }
+  }
+  // zero row BY of every slab: the padded columns of an m-tile window's last
+  // k step (A = 0 there) read it
+  for (int i = threadIdx.x; i < C::NS * C::CS * 3 * SBZ; i += blockDim.x) {
+    const int sl = i / (C::CS * 3 * SBZ), e = i - sl * (C::CS * 3 * SBZ);
+    S.slab[sl][BY * C::CS * 3 * SBZ + e] = 0.0;
   }
   __syncthreads();
   const int lo = S.range[0], nitems = S.range[1] - S.range[0];
@@ -852,23 +869,41 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ>::NW + 1
     }
     cp_async_commit();
   };
+  // psi rows of the current m-tile relative to ITS window: the m-tile's particles
+  // (sorted by xy-cell, Brick::C) span cells ox_m .. ox_m + ex_x of the
+  // sub-brick in x (same in y), so the window is (w + ex_x) x (w + ex_y) columns
+  // from column (ox_m, oy_m) of the sub-brick tile -- 13 x 13 when all 8 share a
+  // cell.  Rows are zero outside the window up to C::FILL entries.
+  int ox_m = 0, oy_m = 0, ex_x = 0, ex_y = 0;
   auto stage = [&](int buf, int cnt) {
-    if (lane < 24) {
-      const int p = lane & 7, d = lane >> 3;
-      const int R = d == 0 ? RX : (d == 1 ? RY : InterpCfg<RX, RY, RZ>::ZP);
-      double* row = wpsi + (d == 0 ? p * C::SX : (d == 1 ? C::OY + p * C::SY : C::OZ + p * C::SZ));
-      constexpr int ZP = InterpCfg<RX, RY, RZ>::ZP;
+    const int p = lane & 7, d = lane >> 3;
+    const bool valid = lane < 24 && p < cnt;
+    int rel = 0;
+    double f = 0.0;
+    if (valid) {
+      const int T0d = d == 0 ? c.T0[0] : (d == 1 ? c.T0[1] : c.T0[2]);
+      double xs = xv[buf][d][p] * g.scale;
+      const int a = anchor_of(xs, g);
+      f = xs - (double)a;
+      rel = a - g.hw - T0d;
+    }
+    int mn = valid ? rel : (1 << 20), mx = valid ? rel : -1;
 #pragma unroll
-      for (int u = 0; u < (RX > ZP ? RX : (RY > ZP ? RY : ZP)); ++u)
-        if (u < R) row[u] = 0.0;
-      if (p < cnt) {
-        const int T0d = d == 0 ? c.T0[0] : (d == 1 ? c.T0[1] : c.T0[2]);
-        double xs = xv[buf][d][p] * g.scale;
-        const int a = anchor_of(xs, g);
-        const double f = xs - (double)a;
-        double* wrow = row + (a - g.hw - T0d);
+    for (int o = 1; o <= 4; o <<= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    ox_m = __shfl_sync(0xffffffffu, mn, 0);
+    oy_m = __shfl_sync(0xffffffffu, mn, 8);
+    ex_x = __shfl_sync(0xffffffffu, mx, 0) - ox_m;
+    ex_y = __shfl_sync(0xffffffffu, mx, 8) - oy_m;
+    if (lane < 24) {
+      double* row = wpsi + (d == 0 ? p * C::SX : (d == 1 ? C::OY + p * C::SY : C::OZ + p * C::SZ));
+#pragma unroll
+      for (int u = 0; u < C::FILL; ++u) row[u] = 0.0;
+      if (valid) {
         const double sv = 2.0 * (f - flo) - 1.0;
-        psi_row(wrow, 0, f, sv, hc, g, two_over_w);
+        psi_row(row + rel - (d == 0 ? ox_m : (d == 1 ? oy_m : 0)), 0, f, sv, hc, g, two_over_w);
       }
     }
   };
@@ -890,8 +925,10 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ>::NW + 1
     for (int nt = 0; nt < C::NT; ++nt) {
       const int zl = 8 * nt + gr;
       Pb[nt] = &S.slab[(c.V + zl / SBZ) % C::NS][0] + (zl % SBZ) +
-               (c.oy * C::CS + c.ox) * 3 * SBZ;
+               ((c.oy + oy_m) * C::CS + c.ox + ox_m) * 3 * SBZ;
     }
+    const int RXm = g.w + ex_x, RYm = g.w + ex_y;  // m-tile window (<= RX x RY)
+    const int KSm = (RXm * RYm + 3) >> 2;
     double acc[C::NT][3][2];
 #pragma unroll
     for (int nt = 0; nt < C::NT; ++nt)
@@ -899,14 +936,14 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ>::NW + 1
       for (int d = 0; d < 3; ++d) acc[nt][d][0] = acc[nt][d][1] = 0.0;
     const double* pxr = wpsi + gr * C::SX;
     const double* pyr = wpsi + C::OY + gr * C::SY;
-    int cx = tq % RX, cy = tq / RX;
+    int cx = tq, cy = 0;  // column 4 ks + tq of the window (RXm >= 4)
 #pragma unroll 2
-    for (int ks = 0; ks < C::KS; ++ks) {
-      const double a = pxr[cx] * pyr[cy];
+    for (int ks = 0; ks < KSm; ++ks) {
+      const double a = pxr[cx] * pyr[cy];  // cy == RYm (last step padding): py = 0
       const int off = (cy * C::CS + cx) * 3 * SBZ;
       cx += 4;
-      if (cx >= RX) {
-        cx -= RX;
+      if (cx >= RXm) {
+        cx -= RXm;
         cy += 1;
       }
 #pragma unroll
@@ -1018,23 +1055,23 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
   return cudaGetLastError();
 }
 
-template <int A, int B, int Cz, int BX, int BY, int SBZ>
+template <int A, int B, int Cz, int BX, int BY, int SBZ, int CSX>
 static cudaError_t interp_slab_launch(unsigned nsub, const double* grid3, double* x, double* v,
                                       int64_t stride, const int* id, double* Eout,
                                       const Sched& offsets, const Brick& g, const Horner& hc,
                                       const PushArgs& P, cudaStream_t st) {
-  using C = SlabCfg<A, B, Cz, BX, BY, SBZ>;
+  using C = SlabCfg<A, B, Cz, BX, BY, SBZ, CSX>;
   const int T = 32 * (C::NW + 1);
-  const size_t smem = sizeof(SlabSmem<A, B, Cz, BX, BY, SBZ>);
+  const size_t smem = sizeof(SlabSmem<A, B, Cz, BX, BY, SBZ, CSX>);
   static int sms = 0;
   if (!sms) {
-    cudaError_t e = cudaFuncSetAttribute(k_interp_push_slab<A, B, Cz, BX, BY, SBZ>,
+    cudaError_t e = cudaFuncSetAttribute(k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, per = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push_slab<A, B, Cz, BX, BY, SBZ>,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX>,
                                                         T, smem);
     if (e != cudaSuccess) return e;
     if (per < 1) return cudaErrorInvalidConfiguration;
@@ -1042,7 +1079,7 @@ static cudaError_t interp_slab_launch(unsigned nsub, const double* grid3, double
   // persistent: one CTA per SM, each with a contiguous run of items
   const unsigned grid = nsub < (unsigned)sms ? nsub : (unsigned)sms;
   if (grid == 0) return cudaSuccess;
-  k_interp_push_slab<A, B, Cz, BX, BY, SBZ><<<grid, T, smem, st>>>(grid3, x, v, stride, id, Eout,
+  k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX><<<grid, T, smem, st>>>(grid3, x, v, stride, id, Eout,
                                                                    offsets, g, hc, P);
   return cudaGetLastError();
 }
@@ -1052,14 +1089,21 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
                                const Horner& hc, const PushArgs& P, cudaStream_t st) {
   const unsigned nsub = (unsigned)offsets.max_i;  // upper bound on interp items
 #ifndef PIF_NO_SLAB
-  if (g.RI[0] == 14 && g.RI[1] == 14 && g.RI[2] == 16 && g.RS[0] == 16 && g.RS[1] == 16 &&
-      g.ib[2] == 4 && g.m[2] == 1)
-    return interp_slab_launch<14, 14, 16, 16, 16, 4>(nsub, grid3, x, v, stride, id, Eout, offsets,
-                                                     g, hc, P, st);
+  // slab-ring kernels (column strides CSX from the bank-conflict search)
+#define PIF_SLAB(A, B, Cz, BX, BY, SBZ, CSX)                                                    \
+  if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz && g.RS[0] == BX && g.RS[1] == BY &&       \
+      g.ib[2] == SBZ && g.m[2] == 1 && (g.C == 1 || g.C == g.ib[0] * g.ib[1]))                 \
+    return interp_slab_launch<A, B, Cz, BX, BY, SBZ, CSX>(nsub, grid3, x, v, stride, id, Eout,   \
+                                                          offsets, g, hc, P, st);
+  PIF_SLAB(14, 14, 16, 16, 16, 4, 18)  // w = 13
+  PIF_SLAB(10, 10, 8, 16, 16, 1, 17)   // w = 8, dense
+  PIF_SLAB(6, 6, 8, 8, 8, 4, 9)        // w = 5, dense
+#undef PIF_SLAB
 #endif
 #define PIF_INTERP(A, B, Cz)                                                                   \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
+  if (g.C != 1) return cudaErrorInvalidValue;  // cell keys need the slab kernel
   PIF_INTERP(6, 6, 8)
   PIF_INTERP(8, 8, 8)
   PIF_INTERP(10, 10, 8)
