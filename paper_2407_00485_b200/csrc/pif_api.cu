@@ -243,7 +243,7 @@ size_t layout(pif_ctx c, char* base) {
   c->soff = (int*)take((c->max_bins + 1) * sizeof(int));
   c->ioff = (int*)take((c->max_bins + 1) * sizeof(int));
   c->moff = (int*)take((c->max_bins + 1) * sizeof(int));
-  c->spart = (int*)take(4 * ((size_t)c->max_bins / 256 + 2) * sizeof(int));
+  c->spart = (int*)take(sched_part_ints(c->max_bins) * sizeof(int));
   c->max_s = c->max_i = 1;
   for (int i = 0; i < 2; ++i) {
     const Plan& p = c->plan[i];
@@ -1201,7 +1201,7 @@ pif_status pif_finalize(pif_ctx c) {
 static pif_status debug_sched(pif_ctx c, const Plan& p, int64_t n, int** counts, Sched& S) {
   const int64_t K = p.nbricks, M = keys_per_brick(p.g);
   const int64_t ms = sched_max_s(K, M, n), mi = sched_max_i(K, n);
-  const size_t ints = K + 4 * (K + 1) + 4 * ((size_t)K / 256 + 2);
+  const size_t ints = K + 4 * (K + 1) + sched_part_ints(K);
   char* buf = nullptr;
   CU(cudaMalloc(&buf, ints * sizeof(int) + 16 + (ms + mi) * sizeof(int4)));
   int* ib = (int*)buf;

@@ -153,14 +153,20 @@ struct Sched {
   int* moff;     // [nkeys + 1] first m-tile (8 particles) of each key
   int4* sitems;  // [max_s]
   int4* iitems;  // [max_i]
-  int* part;     // [4 * nblk_sched(nkeys, M)] scan scratch
+  int* part;     // [sched_part_ints(nkeys)] scan scratch
   int64_t nkeys, max_s, max_i;
 };
 // blocks of the schedule scan (256 bricks each; >= 1)
+#ifndef PIF_SCHED_T
+#define PIF_SCHED_T 64
+#endif
+constexpr int kSchedT = PIF_SCHED_T;  // bricks per schedule-scan block (one thread each)
 inline unsigned nblk_sched(int64_t nkeys, int64_t M) {
-  const int64_t b = (nkeys / M + 255) / 256;
+  const int64_t b = (nkeys / M + kSchedT - 1) / kSchedT;
   return (unsigned)(b < 1 ? 1 : b);
 }
+// ints of scan scratch (Sched::part) for up to nkeys keys
+inline size_t sched_part_ints(int64_t nkeys) { return 4 * ((size_t)nkeys / kSchedT + 2); }
 inline int64_t sched_max_s(int64_t nkeys, int64_t M, int64_t n) { return nkeys / M + n / kSpreadItem + 1; }
 inline int64_t sched_max_i(int64_t nkeys, int64_t n) { return nkeys + n / kInterpItem + 1; }
 

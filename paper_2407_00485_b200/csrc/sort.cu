@@ -48,7 +48,6 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
 // interpolation cost before the group, in m-tiles of 8 particles plus
 // kBrickCost per non-empty brick (the persistent interpolation kernel balances
 // its CTAs' item runs by it); [nkeys] = totals.
-constexpr int kSchedT = 256;
 constexpr int kQ = 4;  // scanned quantities
 // Cost of a non-empty brick's slab loads in the interpolation kernel, in m-tiles
 // (sparse regions: one m-tile per brick would otherwise look free)
