@@ -202,7 +202,7 @@ struct pif_ctx_s {
   double *xA = nullptr, *vA = nullptr, *xB = nullptr, *vB = nullptr;
   int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *counts = nullptr,
       *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr, *moff = nullptr, *spart = nullptr;
-  int4 *sitems = nullptr, *iitems = nullptr;
+  int4 *sitems = nullptr, *iitems = nullptr, *iinfo = nullptr;
   int64_t max_s = 1, max_i = 1;
   double *partials = nullptr, *red = nullptr;
   void* fft_work = nullptr;
@@ -254,6 +254,7 @@ size_t layout(pif_ctx c, char* base) {
   }
   c->sitems = (int4*)take(c->max_s * sizeof(int4));
   c->iitems = (int4*)take(c->max_i * sizeof(int4));
+  c->iinfo = (int4*)take(c->max_i * sizeof(int4));
   c->flag = (int*)take(64);
   c->partials = (double*)take(4 * kReduceBlocks * sizeof(double));
   c->red = (double*)take(16 * sizeof(double));
@@ -456,7 +457,7 @@ pif_status ph_mark(pif_ctx c, int ph) {
 
 Sched sched_of(pif_ctx c, const Plan& p) {
   const int64_t M = keys_per_brick(p.g);
-  return Sched{c->offsets, c->soff, c->ioff, c->moff, c->sitems, c->iitems, c->spart, p.nbricks,
+  return Sched{c->offsets, c->soff, c->ioff, c->moff, c->sitems, c->iitems, c->iinfo, c->spart, p.nbricks,
                sched_max_s(p.nbricks, M, c->nloc), sched_max_i(p.nbricks, c->nloc)};
 }
 
@@ -465,7 +466,7 @@ pif_status sort_particles(pif_ctx c, Plan& p) {
   const int64_t n = c->nloc;
   CU(cudaMemsetAsync(c->counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(c->xA, n, n, p.g, c->key, c->rnk, c->counts, c->st));
-  CU(launch_schedule(c->counts, sched_of(c, p), keys_per_brick(p.g), p.g.C, c->st));
+  CU(launch_schedule(c->counts, sched_of(c, p), p.g, keys_per_brick(p.g), p.g.C, c->st));
   CU(launch_scatter_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->xB,
                            c->vB, c->idB, nullptr, c->st));
   std::swap(c->xA, c->xB);
@@ -1203,12 +1204,12 @@ static pif_status debug_sched(pif_ctx c, const Plan& p, int64_t n, int** counts,
   const int64_t ms = sched_max_s(K, M, n), mi = sched_max_i(K, n);
   const size_t ints = K + 4 * (K + 1) + sched_part_ints(K);
   char* buf = nullptr;
-  CU(cudaMalloc(&buf, ints * sizeof(int) + 16 + (ms + mi) * sizeof(int4)));
+  CU(cudaMalloc(&buf, ints * sizeof(int) + 16 + (ms + 2 * mi) * sizeof(int4)));
   int* ib = (int*)buf;
   *counts = ib;
   int4* items = (int4*)(((uintptr_t)(ib + ints) + 15) & ~(uintptr_t)15);
-  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, ib + 4 * K + 3, items, items + ms, ib + 5 * K + 4,
-            K, ms, mi};
+  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, ib + 4 * K + 3, items, items + ms, items + ms + mi,
+            ib + 5 * K + 4, K, ms, mi};
   return PIF_OK;
 }
 pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, const double* s,
@@ -1239,7 +1240,7 @@ pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, con
   CU(launch_iota(id, n, c->st));
   CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_schedule(counts, S, keys_per_brick(p.g), p.g.C, c->st));
+  CU(launch_schedule(counts, S, p.g, keys_per_brick(p.g), p.g.C, c->st));
   CU(launch_scatter_sorted(dx, nullptr, id, ds, n, n, key, rk, offs, dx2, nullptr, id2, ds2, c->st));
   CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
   CU(launch_spread(dx2, n, ds2, 1.0, S, p.g, p.hc, p.grid, c->st));
@@ -1278,7 +1279,7 @@ pif_status pif_debug_type2(pif_ctx c, int which, const double* cin, const double
   CU(launch_iota(id, n, c->st));
   CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_schedule(counts, S, keys_per_brick(p.g), p.g.C, c->st));
+  CU(launch_schedule(counts, S, p.g, keys_per_brick(p.g), p.g.C, c->st));
   CU(launch_scatter_sorted(dx, nullptr, id, nullptr, n, n, key, rk, offs, dx2, nullptr, id2, nullptr, c->st));
   CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, c->st));
   CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3));

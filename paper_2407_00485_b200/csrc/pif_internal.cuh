@@ -150,13 +150,14 @@ struct Sched {
   int* offsets;  // [nkeys + 1]
   int* soff;     // [nkeys + 1]
   int* ioff;     // [nkeys + 1]
-  int* moff;     // [nkeys + 1] first m-tile (8 particles) of each key
+  int* moff;     // [nkeys + 1] interpolation cost (m-tiles + brick loads) before each key
   int4* sitems;  // [max_s]
   int4* iitems;  // [max_i]
+  int4* iinfo;   // [max_i] decoded interp item: {bx, by, bz, sx | sy << 16}
   int* part;     // [sched_part_ints(nkeys)] scan scratch
   int64_t nkeys, max_s, max_i;
 };
-// blocks of the schedule scan (256 bricks each; >= 1)
+// blocks of the schedule scan (kSchedT bricks each; >= 1)
 #ifndef PIF_SCHED_T
 #define PIF_SCHED_T 64
 #endif
@@ -174,7 +175,8 @@ inline int64_t sched_max_i(int64_t nkeys, int64_t n) { return nkeys + n / kInter
 // All launchers enqueue on `st` and return cudaGetLastError().
 cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const Brick& g, int* key,
                              int* rank, int* counts, cudaStream_t st);
-cudaError_t launch_schedule(const int* counts, const Sched& S, int M, int C, cudaStream_t st);
+cudaError_t launch_schedule(const int* counts, const Sched& S, const Brick& g, int M, int C,
+                            cudaStream_t st);
 // keys per spreading brick
 inline int keys_per_brick(const Brick& g) { return g.m[0] * g.m[1] * g.m[2] * g.C; }
 cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,

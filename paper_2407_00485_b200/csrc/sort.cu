@@ -200,16 +200,25 @@ __global__ void __launch_bounds__(kSchedT) k_sched_apply(const int* __restrict__
 
 // One thread per key: (first key of a group) the interp items of the group,
 // and (first key of a brick) the spread items of the brick.
-__global__ void k_schedule_fill(Sched S, int M, int C) {
+__global__ void k_schedule_fill(Sched S, Brick g, int M, int C) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= S.nkeys) return;
   const int a = S.offsets[k];
   if (k % C == 0) {
     const int b = S.offsets[k + C];
     int it = S.ioff[k];
+    // decoded brick / sub-brick coordinates (the slab kernel's item cursors then
+    // need no integer divisions)
+    const int Ms = g.m[0] * g.m[1] * g.m[2];
+    const int brick = (int)(k / M), sk = (int)((k / C) % Ms);
+    const int bz = brick % g.NB[2], by = (brick / g.NB[2]) % g.NB[1], bx = brick / (g.NB[2] * g.NB[1]);
+    const int sy = (sk / g.m[2]) % g.m[1], sx = sk / (g.m[2] * g.m[1]);
+    const int4 info = make_int4(bx, by, bz, sx | (sy << 16));
     // .w = the item's cost offset (m-tiles, key order)
-    for (int s0 = a; s0 < b; s0 += kInterpItem)
+    for (int s0 = a; s0 < b; s0 += kInterpItem) {
+      S.iinfo[it] = info;
       S.iitems[it++] = make_int4((int)k, s0, min(b, s0 + kInterpItem), S.moff[k] + ((s0 - a) >> 3));
+    }
   }
   if (k % M == 0) {
     const int e = S.offsets[k + M];
@@ -263,12 +272,13 @@ cudaError_t launch_bin_count(const double* x, int64_t stride, int64_t n, const B
   if (n > 0) k_bin_count<<<nblk(n, 256), 256, 0, st>>>(x, stride, n, g, key, rank, counts);
   return cudaGetLastError();
 }
-cudaError_t launch_schedule(const int* counts, const Sched& S, int M, int C, cudaStream_t st) {
+cudaError_t launch_schedule(const int* counts, const Sched& S, const Brick& g, int M, int C,
+                            cudaStream_t st) {
   const unsigned nsb = nblk_sched(S.nkeys, M);
   k_sched_reduce<<<nsb, kSchedT, 0, st>>>(counts, S, M, C);
   k_sched_partials<<<1, 1024, 0, st>>>(S, (int)nsb);
   k_sched_apply<<<nsb, kSchedT, 0, st>>>(counts, S, M, C);
-  k_schedule_fill<<<nblk(S.nkeys, 256), 256, 0, st>>>(S, M, C);
+  k_schedule_fill<<<nblk(S.nkeys, 256), 256, 0, st>>>(S, g, M, C);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,

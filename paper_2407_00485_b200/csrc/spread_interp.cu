@@ -228,7 +228,7 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
     const int R = d == 0 ? RX : (d == 1 ? RY : (RZ + 7) / 8 * 8);
     double* row = d == 0 ? sm.px[p] : (d == 1 ? sm.py[p] : sm.pz[p]);
     if (p >= cnt) {
-      for (int u = 0; u < R; ++u) row[u] = 0.0;
+      for (int u = 0; u < R + (d == 1 && RX * RY % 8 != 0 ? 1 : 0); ++u) row[u] = 0.0;
       continue;
     }
     const int rel = sm.rel[p][d];
@@ -236,6 +236,7 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
     const double f = sm.xs[p][d] - (double)(rel + g.hw + T0d);  // x~ - anchor
     for (int u = 0; u < rel; ++u) row[u] = 0.0;
     for (int u = rel + w; u < R; ++u) row[u] = 0.0;
+    if (d == 1 && RX * RY % 8 != 0) row[R] = 0.0;  // padded spread columns read py[RY]
     const double sv = 2.0 * (f - flo) - 1.0;
     psi_row(row, rel, f, sv, hc, g, two_over_w);
   }
@@ -245,14 +246,18 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
 // ------------------------------------------------------------------ spread --
 template <int RX, int RY, int RZ>
 struct SpreadCfg {
-  static constexpr int NCT = RX * RY / 8;         // column tiles (of 8)
-  static constexpr int CT = NCT % 4 == 0 ? 4 : 3; // column tiles per warp
+  static constexpr int NCT = (RX * RY + 7) / 8;   // column tiles (of 8; the last may be padded)
+  static constexpr int CT = NCT % 4 == 0 ? 4 : (NCT % 5 == 0 ? 5 : 3);  // column tiles per warp
   static constexpr int NW = NCT / CT;             // warps
   static constexpr int ZT = (RZ + 7) / 8;         // z tiles of 8 (psi_z rows zero-padded)
-  static_assert(RX * RY % 8 == 0 && NCT % CT == 0, "tile shape");
+  static constexpr bool PADC = RX * RY % 8 != 0;  // padded columns c >= RX RY (A = 0: py row RY)
+  static_assert(NCT % CT == 0, "tile shape");
 };
 
-template <int RX, int RY, int RZ, bool HAS_S>
+// SUB: one CTA per interpolation item (a sub-brick's particles, tile RI)
+// instead of per brick (tile RS): fewer padded FMAs per particle, more
+// REDG.ADD.F64 per particle in the flush.
+template <int RX, int RY, int RZ, bool HAS_S, bool SUB>
 __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, PIF_SPREAD_MINB)
     k_spread(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
              double s_uniform, const Sched Sc, Brick g,
@@ -262,7 +267,17 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, PIF_SPREAD_MIN
   Psi<RX, RY, RZ>& sm = *reinterpret_cast<Psi<RX, RY, RZ>*>(smem_raw);
   int T0[3];
   int64_t start, end;
-  if (!tile_of(g, Sc, false, T0, start, end)) return;
+  if (SUB) {
+    if ((int)blockIdx.x >= Sc.ioff[Sc.nkeys]) return;
+    const int4 e = Sc.iitems[blockIdx.x];
+    const int4 f = Sc.iinfo[blockIdx.x];  // {bx, by, bz, sx | sy << 16}
+    start = e.y;
+    end = e.z;
+    T0[0] = f.x * g.sb[0] - g.hw + (f.w & 0xffff) * g.ib[0];
+    T0[1] = f.y * g.sb[1] - g.hw + (f.w >> 16) * g.ib[1];
+    T0[2] = f.z * g.sb[2] - g.hw;
+    if (start >= end) return;
+  } else if (!tile_of(g, Sc, false, T0, start, end)) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gr = lane >> 2, tq = lane & 3;
   // A-fragment rows: column c = (wid*CT + ct)*8 + gr
@@ -316,7 +331,8 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, PIF_SPREAD_MIN
       for (int i = 0; i < 2; ++i) {
         const double val = acc[ct][zt][i];
         const int z = zt * 8 + 2 * tq + i;
-        if (z < RZ && val != 0.0) atomicAdd(colp + wrapi(T0[2] + z, n), val * s_uniform);
+        if (z < RZ && val != 0.0 && (!C::PADC || acy[ct] < RY))
+          atomicAdd(colp + wrapi(T0[2] + z, n), val * s_uniform);
       }
   }
 }
@@ -707,14 +723,12 @@ template <int NSZ>
 __device__ __forceinline__ void slab_cursor_load(SlabCursor& it, int lo, const Brick& g,
                                                  const Sched& Sc) {
   const int4 e = Sc.iitems[lo + it.k];
+  const int4 f = Sc.iinfo[lo + it.k];  // {bx, by, bz, sx | sy << 16}
   it.start = e.y;
   it.end = e.z;
   it.m = (int)((e.z - e.y + 7) >> 3);
-  const int M = g.m[0] * g.m[1] * g.m[2];
-  const int brick = e.x / (M * g.C), sk = (e.x / g.C) % M;  // e.x: the sub-brick's first key
-  const int bz = brick % g.NB[2], bcol = brick / g.NB[2];
-  const int by = bcol % g.NB[1], bx = bcol / g.NB[1];
-  const int sy = (sk / g.m[2]) % g.m[1], sx = sk / (g.m[2] * g.m[1]);
+  const int bx = f.x, by = f.y, bz = f.z, sx = f.w & 0xffff, sy = f.w >> 16;
+  const int bcol = bx * g.NB[1] + by;
   it.ox = sx * g.ib[0];
   it.oy = sy * g.ib[1];
   it.T0[0] = bx * g.sb[0] - g.hw + it.ox;
@@ -991,7 +1005,7 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>::N
   cp_async_wait_all();
 }
 
-template <int A, int B, int Cz>
+template <int A, int B, int Cz, bool SUB = false>
 static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, const double* s,
                                  double s_uniform, const Sched& offsets, const Brick& g,
                                  const Horner& hc, double* grid, cudaStream_t st) {
@@ -999,24 +1013,30 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
   const size_t smem = sizeof(Psi<A, B, Cz, kChunk>);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_spread<A, B, Cz, true>,
+    cudaError_t e = cudaFuncSetAttribute(k_spread<A, B, Cz, true, SUB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_spread<A, B, Cz, false>,
+      e = cudaFuncSetAttribute(k_spread<A, B, Cz, false, SUB>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   if (s)
-    k_spread<A, B, Cz, true><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread<A, B, Cz, true, SUB><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
   else
-    k_spread<A, B, Cz, false><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread<A, B, Cz, false, SUB><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
   return cudaGetLastError();
 }
 
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
                           const Sched& offsets, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st) {
+#ifdef PIF_SPREAD_SUB
+  // sub-brick spreading on the interpolation items (w = 13 tile, cell keys)
+  if (g.RI[0] == 14 && g.RI[1] == 14 && g.RI[2] == 16 && g.C > 1)
+    return spread_launch<14, 14, 16, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
+                                           g, hc, grid, st);
+#endif
   const unsigned nbr = (unsigned)offsets.max_s;  // upper bound on spread items
 #define PIF_SPREAD(A, B, Cz)                                        \
   if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz)                \

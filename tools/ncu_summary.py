@@ -2,7 +2,7 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) and one
 `ncu --set full` report into profiles/:
 
-  python tools/ncu_summary.py LAUNCHES.csv REPORT.ncu-rep TAG
+  python tools/ncu_summary.py LAUNCHES.csv REPORT.ncu-rep TAG [MORE.ncu-rep ...]
 
 writes profiles/<TAG>_launches.md (per-kernel time shares of the step),
 profiles/<TAG>_ncu_full.md (key metrics per profiled kernel) and
@@ -25,7 +25,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
-SHORT = {"k_interp_push": "interp_push", "k_spread": "spread"}
+SHORT = {"k_interp_push": "interp_push", "k_spread": "spread", "k_bin_count": "bin_count",
+         "k_scatter_sorted": "scatter_sorted"}
 
 
 def launches(path):
@@ -65,6 +66,7 @@ def to_bytes(val, unit):
 
 def main():
     lpath, rpath, tag = sys.argv[1:4]
+    extra = sys.argv[4:]
     agg, unit = launches(lpath)
     tot = sum(v[1] for v in agg.values())
     lines = [f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)",
@@ -74,6 +76,8 @@ def main():
         lines.append(f"| `{k[:70]}` | {n} | {v:.0f} {unit} | {100 * v / tot:.1f} % |")
     open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
     rep = full(rpath)
+    for e in extra:
+        rep += full(e)
     lines = [f"# {tag}: `ncu --set full` key metrics", ""]
     traffic = {}
     for name, m in rep:
