@@ -672,7 +672,11 @@ struct SlabCfg {
   // doubles per slab: BY + 1 rows (the last one zero); one-row slabs (SBZ = 1)
   // are padded to 4 (mod 16) so that the 4 slabs of a half-warp's fragment rows
   // fall in different banks (conflict pattern checked exhaustively)
-  static constexpr int SLAB0 = (BY + 1) * CS * 3 * SBZ;
+#ifndef PIF_SLAB_ZROW
+#define PIF_SLAB_ZROW 1
+#endif
+  static constexpr int ZROW = PIF_SLAB_ZROW;        // + a zero row per slab
+  static constexpr int SLAB0 = (BY + ZROW) * CS * 3 * SBZ;
   static constexpr int SLAB = SBZ == 1 ? SLAB0 + ((20 - SLAB0 % 16) % 16) : SLAB0;
   static constexpr int NSZ = RZ / SBZ;              // slabs per tile
   static constexpr int ND = 16;                     // full / done barrier ring
@@ -777,11 +781,19 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>::N
       mbar_init(&S.done[b], C::NW);
     }
   }
-  // zero row BY of every slab: the padded columns of an m-tile window's last
-  // k step (A = 0 there) read it
-  for (int i = threadIdx.x; i < C::NS * C::CS * 3 * SBZ; i += blockDim.x) {
-    const int sl = i / (C::CS * 3 * SBZ), e = i - sl * (C::CS * 3 * SBZ);
-    S.slab[sl][BY * C::CS * 3 * SBZ + e] = 0.0;
+  // The padded columns of an m-tile window's last k step (A = 0 there) read row
+  // BY of their slab: a zero row (ZROW), or else the next slab / the psi rows,
+  // which hold finite values once the whole buffer is zeroed here (a read racing
+  // a cp.async still combines finite halves: the high word carries the exponent)
+  if (C::ZROW) {
+    for (int i = threadIdx.x; i < C::NS * C::CS * 3 * SBZ; i += blockDim.x) {
+      const int sl = i / (C::CS * 3 * SBZ), e = i - sl * (C::CS * 3 * SBZ);
+      S.slab[sl][BY * C::CS * 3 * SBZ + e] = 0.0;
+    }
+  } else {
+    double2* z = reinterpret_cast<double2*>(&S.slab[0][0]);
+    const int n2 = (int)((sizeof(S.slab) + sizeof(S.psi)) / sizeof(double2));
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) z[i] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   const int lo = S.range[0], nitems = S.range[1] - S.range[0];
@@ -1115,7 +1127,10 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
       g.ib[2] == SBZ && g.m[2] == 1 && (g.C == 1 || g.C == g.ib[0] * g.ib[1]))                 \
     return interp_slab_launch<A, B, Cz, BX, BY, SBZ, CSX>(nsub, grid3, x, v, stride, id, Eout,   \
                                                           offsets, g, hc, P, st);
-  PIF_SLAB(14, 14, 16, 16, 16, 4, 18)  // w = 13
+#ifndef PIF_SLAB13_CS
+#define PIF_SLAB13_CS 18
+#endif
+  PIF_SLAB(14, 14, 16, 16, 16, 4, PIF_SLAB13_CS)  // w = 13
   PIF_SLAB(10, 10, 8, 16, 16, 1, 17)   // w = 8, dense
   PIF_SLAB(6, 6, 8, 8, 8, 4, 9)        // w = 5, dense
 #undef PIF_SLAB
