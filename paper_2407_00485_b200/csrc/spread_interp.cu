@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
 // Slab layout: [cy * CS + cx][d][r] (r < SBZ rows), CS = 18 for BX = 16: the
 // B-fragment reads (lane (g, t): tile row 8 nt + g, sub-window column 4 ks + t)
 // are conflict-free for every sub-brick offset (checked exhaustively).
-template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX>
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX, int ZR>
 struct SlabCfg {
   using I = InterpCfg<RX, RY, RZ>;
   static constexpr int KS = I::KS, NT = I::NT;
@@ -672,19 +672,18 @@ struct SlabCfg {
   // doubles per slab: BY + 1 rows (the last one zero); one-row slabs (SBZ = 1)
   // are padded to 4 (mod 16) so that the 4 slabs of a half-warp's fragment rows
   // fall in different banks (conflict pattern checked exhaustively)
-#ifndef PIF_SLAB_ZROW
-#define PIF_SLAB_ZROW 1
-#endif
-  static constexpr int ZROW = PIF_SLAB_ZROW;        // + a zero row per slab
+  static constexpr int ZROW = ZR;                   // + a zero row per slab
   static constexpr int SLAB0 = (BY + ZROW) * CS * 3 * SBZ;
   static constexpr int SLAB = SBZ == 1 ? SLAB0 + ((20 - SLAB0 % 16) % 16) : SLAB0;
   static constexpr int NSZ = RZ / SBZ;              // slabs per tile
   static constexpr int ND = 16;                     // full / done barrier ring
 #ifndef PIF_SLAB_NS
-#define PIF_SLAB_NS 5
+#define PIF_SLAB_NS 6
 #endif
   // slab ring: a tile plus the lookahead (brick steps along z)
   static constexpr int NS = NSZ == 4 ? PIF_SLAB_NS : (SBZ == 1 ? NSZ + 4 : NSZ + 2);
+  static_assert(ZR == 1 || NS * (BY * CSX * 3 * SBZ) * 8 + 8 * (WP + 96) * 16 <= 232448 - 512,
+                "ring too large");
 #ifndef PIF_SLAB_NW
 #define PIF_SLAB_NW 16
 #endif
@@ -702,9 +701,9 @@ struct SlabCfg {
   static_assert(NW >= 8, "slab ring too large");
 };
 
-template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX>
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX, int ZR>
 struct SlabSmem {
-  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>;
+  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR>;
   double slab[C::NS][C::SLAB];
   double psi[C::NW][C::WP];
   double xv[C::NW][2][6][8];
@@ -746,15 +745,15 @@ __device__ __forceinline__ void slab_cursor_load(SlabCursor& it, int lo, const B
   it.bz = bz;
 }
 
-template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX>
-__global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>::NW + 1), 1)
+template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX, int ZR>
+__global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR>::NW + 1), 1)
     k_interp_push_slab(const double* __restrict__ grid3, double* __restrict__ x,
                        double* __restrict__ v, int64_t stride, const int* __restrict__ id,
                        double* __restrict__ Eout, const Sched Sc, Brick g,
                        const __grid_constant__ Horner hc, PushArgs P) {
-  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX>;
+  using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SlabSmem<RX, RY, RZ, BX, BY, SBZ, CSX>& S = *reinterpret_cast<SlabSmem<RX, RY, RZ, BX, BY, SBZ, CSX>*>(smem_raw);
+  SlabSmem<RX, RY, RZ, BX, BY, SBZ, CSX, ZR>& S = *reinterpret_cast<SlabSmem<RX, RY, RZ, BX, BY, SBZ, CSX, ZR>*>(smem_raw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n = g.n;
   const int64_t n3 = (int64_t)n * n * n;
@@ -1087,23 +1086,23 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
   return cudaGetLastError();
 }
 
-template <int A, int B, int Cz, int BX, int BY, int SBZ, int CSX>
+template <int A, int B, int Cz, int BX, int BY, int SBZ, int CSX, int ZR>
 static cudaError_t interp_slab_launch(unsigned nsub, const double* grid3, double* x, double* v,
                                       int64_t stride, const int* id, double* Eout,
                                       const Sched& offsets, const Brick& g, const Horner& hc,
                                       const PushArgs& P, cudaStream_t st) {
-  using C = SlabCfg<A, B, Cz, BX, BY, SBZ, CSX>;
+  using C = SlabCfg<A, B, Cz, BX, BY, SBZ, CSX, ZR>;
   const int T = 32 * (C::NW + 1);
-  const size_t smem = sizeof(SlabSmem<A, B, Cz, BX, BY, SBZ, CSX>);
+  const size_t smem = sizeof(SlabSmem<A, B, Cz, BX, BY, SBZ, CSX, ZR>);
   static int sms = 0;
   if (!sms) {
-    cudaError_t e = cudaFuncSetAttribute(k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX>,
+    cudaError_t e = cudaFuncSetAttribute(k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX, ZR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, per = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX>,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX, ZR>,
                                                         T, smem);
     if (e != cudaSuccess) return e;
     if (per < 1) return cudaErrorInvalidConfiguration;
@@ -1111,7 +1110,7 @@ static cudaError_t interp_slab_launch(unsigned nsub, const double* grid3, double
   // persistent: one CTA per SM, each with a contiguous run of items
   const unsigned grid = nsub < (unsigned)sms ? nsub : (unsigned)sms;
   if (grid == 0) return cudaSuccess;
-  k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX><<<grid, T, smem, st>>>(grid3, x, v, stride, id, Eout,
+  k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX, ZR><<<grid, T, smem, st>>>(grid3, x, v, stride, id, Eout,
                                                                    offsets, g, hc, P);
   return cudaGetLastError();
 }
@@ -1122,17 +1121,14 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
   const unsigned nsub = (unsigned)offsets.max_i;  // upper bound on interp items
 #ifndef PIF_NO_SLAB
   // slab-ring kernels (column strides CSX from the bank-conflict search)
-#define PIF_SLAB(A, B, Cz, BX, BY, SBZ, CSX)                                                    \
+#define PIF_SLAB(A, B, Cz, BX, BY, SBZ, CSX, ZR)                                                \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz && g.RS[0] == BX && g.RS[1] == BY &&       \
       g.ib[2] == SBZ && g.m[2] == 1 && (g.C == 1 || g.C == g.ib[0] * g.ib[1]))                 \
-    return interp_slab_launch<A, B, Cz, BX, BY, SBZ, CSX>(nsub, grid3, x, v, stride, id, Eout,   \
-                                                          offsets, g, hc, P, st);
-#ifndef PIF_SLAB13_CS
-#define PIF_SLAB13_CS 18
-#endif
-  PIF_SLAB(14, 14, 16, 16, 16, 4, PIF_SLAB13_CS)  // w = 13
-  PIF_SLAB(10, 10, 8, 16, 16, 1, 17)   // w = 8, dense
-  PIF_SLAB(6, 6, 8, 8, 8, 4, 9)        // w = 5, dense
+    return interp_slab_launch<A, B, Cz, BX, BY, SBZ, CSX, ZR>(nsub, grid3, x, v, stride, id,     \
+                                                              Eout, offsets, g, hc, P, st);
+  PIF_SLAB(14, 14, 16, 16, 16, 4, 17, 0)  // w = 13: ring of 6 slabs without zero rows
+  PIF_SLAB(10, 10, 8, 16, 16, 1, 17, 1)   // w = 8, dense
+  PIF_SLAB(6, 6, 8, 8, 8, 4, 9, 1)        // w = 5, dense
 #undef PIF_SLAB
 #endif
 #define PIF_INTERP(A, B, Cz)                                                                   \
