@@ -211,6 +211,19 @@ __device__ __forceinline__ void psi_row(double* row, int rel, double f, double s
   }
 }
 
+// Column tiles of 8 of a spreading tile: ceil(RX RY / 8), or more (padded) when
+// that gives more column tiles per warp (PIF_SPREAD_NCT13 for the 10x10 tile)
+#ifndef PIF_SPREAD_NCT13
+#define PIF_SPREAD_NCT13 13
+#endif
+__host__ __device__ constexpr int spread_nct(int RX, int RY) {
+  return (RX * RY + 7) / 8 == 13 ? PIF_SPREAD_NCT13 : (RX * RY + 7) / 8;
+}
+// py entries past RY that padded columns c >= RX RY read (A = 0 there)
+__host__ __device__ constexpr int spread_pad_rows(int RX, int RY) {
+  return (spread_nct(RX, RY) * 8 + RX - 1) / RX - RY;
+}
+
 // ES weights of the chunk's particles (positions already staged); particles
 // cnt .. pad-1 get zero rows.  One item per (dimension, particle): the w window
 // weights by per-node Horner polynomials (edge nodes exactly), zeros elsewhere
@@ -228,7 +241,7 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
     const int R = d == 0 ? RX : (d == 1 ? RY : (RZ + 7) / 8 * 8);
     double* row = d == 0 ? sm.px[p] : (d == 1 ? sm.py[p] : sm.pz[p]);
     if (p >= cnt) {
-      for (int u = 0; u < R + (d == 1 && RX * RY % 8 != 0 ? 1 : 0); ++u) row[u] = 0.0;
+      for (int u = 0; u < R + (d == 1 ? spread_pad_rows(RX, RY) : 0); ++u) row[u] = 0.0;
       continue;
     }
     const int rel = sm.rel[p][d];
@@ -236,7 +249,8 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
     const double f = sm.xs[p][d] - (double)(rel + g.hw + T0d);  // x~ - anchor
     for (int u = 0; u < rel; ++u) row[u] = 0.0;
     for (int u = rel + w; u < R; ++u) row[u] = 0.0;
-    if (d == 1 && RX * RY % 8 != 0) row[R] = 0.0;  // padded spread columns read py[RY]
+    if (d == 1)  // padded spread columns read py[RY ..]
+      for (int u = R; u < R + spread_pad_rows(RX, RY); ++u) row[u] = 0.0;
     const double sv = 2.0 * (f - flo) - 1.0;
     psi_row(row, rel, f, sv, hc, g, two_over_w);
   }
@@ -246,11 +260,15 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
 // ------------------------------------------------------------------ spread --
 template <int RX, int RY, int RZ>
 struct SpreadCfg {
-  static constexpr int NCT = (RX * RY + 7) / 8;   // column tiles (of 8; the last may be padded)
-  static constexpr int CT = NCT % 4 == 0 ? 4 : (NCT % 5 == 0 ? 5 : 3);  // column tiles per warp
+  static constexpr int NCT = spread_nct(RX, RY);   // column tiles (of 8; the last ones may be padded)
+  // column tiles per warp: 4 (or 5, 3) when that leaves >= 4 warps, else 1
+  static constexpr int CT = (NCT % 4 == 0 && NCT >= 16) ? 4
+                            : (NCT % 5 == 0 && NCT >= 20) ? 5
+                            : (NCT % 3 == 0 && NCT >= 12) ? 3 : 1;
   static constexpr int NW = NCT / CT;             // warps
   static constexpr int ZT = (RZ + 7) / 8;         // z tiles of 8 (psi_z rows zero-padded)
-  static constexpr bool PADC = RX * RY % 8 != 0;  // padded columns c >= RX RY (A = 0: py row RY)
+  static constexpr bool PADC = NCT * 8 != RX * RY;  // padded columns c >= RX RY (A = 0: py rows >= RY)
+  static_assert(RY + spread_pad_rows(RX, RY) <= RowStride<RY>::v, "py row stride");
   static_assert(NCT % CT == 0, "tile shape");
 };
 
@@ -1047,6 +1065,18 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
   if (g.RI[0] == 14 && g.RI[1] == 14 && g.RI[2] == 16 && g.C > 1)
     return spread_launch<14, 14, 16, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
                                            g, hc, grid, st);
+#endif
+#ifndef PIF_NO_SPREAD_SUB_DENSE
+  // dense w = 8 / w = 5 plans (>= 12 / 8 particles per cell, cell keys): spread
+  // over the interpolation sub-bricks with the interpolation tile (10x10x8 /
+  // 6x6x8 instead of 16x16x8 / 8^3: 2.6x / 1.8x fewer padded FMAs), the extra
+  // REDG flush per particle being small at that density
+  if (g.C > 1 && g.RI[0] == 10 && g.RI[1] == 10 && g.RI[2] == 8)
+    return spread_launch<10, 10, 8, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
+                                          g, hc, grid, st);
+  if (g.C > 1 && g.RI[0] == 6 && g.RI[1] == 6 && g.RI[2] == 8)
+    return spread_launch<6, 6, 8, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
+                                        g, hc, grid, st);
 #endif
   const unsigned nbr = (unsigned)offsets.max_s;  // upper bound on spread items
 #define PIF_SPREAD(A, B, Cz)                                        \
