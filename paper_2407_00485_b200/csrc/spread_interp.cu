@@ -707,7 +707,11 @@ struct SlabCfg {
 #endif
   static constexpr int BYTES = 232448 - 2 * ND * 8 - 64;
   static constexpr int NWFIT = (BYTES / 8 - NS * SLAB) / (WP + 96);
-  static constexpr int NW = NWFIT < PIF_SLAB_NW ? NWFIT : PIF_SLAB_NW;
+#ifndef PIF_SLAB_NW1
+#define PIF_SLAB_NW1 16  // one-row slabs (w = 8 dense)
+#endif
+  static constexpr int NWCAP = SBZ == 1 ? PIF_SLAB_NW1 : PIF_SLAB_NW;
+  static constexpr int NW = NWFIT < NWCAP ? NWFIT : NWCAP;
   // psi rows are zero-filled to FILL entries (px < RX, py <= RY: the padded
   // columns of a window's last k step, pz < ZP)
   static constexpr int FILL0 = RX > RY + 1 ? RX : RY + 1;
