@@ -39,7 +39,8 @@ CONFIGS = {1: ("landau", 32, 1 << 21, 1e-12, 0.05),     # C2
            3: ("penning", 64, 1 << 24, 1e-12, 0.003125),  # C4 (Boris push)
            4: ("landau", 64, 1 << 26, 1e-7, 0.003125),    # C5 fine propagator (1 GPU)
            5: ("landau", 64, 1 << 22, 1e-7, 0.003125),    # C5-reduced parareal fine propagator
-           6: ("landau", 64, 1 << 22, 1e-4, 0.05)}        # C5-reduced parareal coarse (PIF) propagator
+           6: ("landau", 64, 1 << 22, 1e-4, 0.05),        # C5-reduced parareal coarse (PIF) propagator
+           7: ("landau", 64, 1 << 26, 1e-4, 0.05)}        # C5 coarse (PIF, eps 1e-4) propagator (1 GPU)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 SM_COUNT = 148

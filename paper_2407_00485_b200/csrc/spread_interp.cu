@@ -710,7 +710,10 @@ struct SlabCfg {
 #ifndef PIF_SLAB_NW1
 #define PIF_SLAB_NW1 24  // one-row slabs (w = 8 dense: smaller psi rows, 80 registers)
 #endif
-  static constexpr int NWCAP = SBZ == 1 ? PIF_SLAB_NW1 : PIF_SLAB_NW;
+#ifndef PIF_SLAB_NW2
+#define PIF_SLAB_NW2 16  // two-slab tiles (w = 5 dense)
+#endif
+  static constexpr int NWCAP = SBZ == 1 ? PIF_SLAB_NW1 : (NSZ == 2 ? PIF_SLAB_NW2 : PIF_SLAB_NW);
   static constexpr int NW = NWFIT < NWCAP ? NWFIT : NWCAP;
   // psi rows are zero-filled to FILL entries (px < RX, py <= RY: the padded
   // columns of a window's last k step, pz < ZP)
