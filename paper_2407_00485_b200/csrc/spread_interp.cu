@@ -711,7 +711,7 @@ struct SlabCfg {
 #define PIF_SLAB_NW1 24  // one-row slabs (w = 8 dense: smaller psi rows, 80 registers)
 #endif
 #ifndef PIF_SLAB_NW2
-#define PIF_SLAB_NW2 16  // two-slab tiles (w = 5 dense)
+#define PIF_SLAB_NW2 24  // two-slab tiles (w = 5 dense)
 #endif
   static constexpr int NWCAP = SBZ == 1 ? PIF_SLAB_NW1 : (NSZ == 2 ? PIF_SLAB_NW2 : PIF_SLAB_NW);
   static constexpr int NW = NWFIT < NWCAP ? NWFIT : NWCAP;
