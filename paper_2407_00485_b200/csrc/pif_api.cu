@@ -200,7 +200,7 @@ struct pif_ctx_s {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   double *xA = nullptr, *vA = nullptr, *xB = nullptr, *vB = nullptr;
-  int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *counts = nullptr,
+  int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *perm = nullptr, *counts = nullptr,
       *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr, *moff = nullptr, *spart = nullptr;
   int4 *sitems = nullptr, *iitems = nullptr, *iinfo = nullptr;
   int64_t max_s = 1, max_i = 1;
@@ -238,6 +238,7 @@ size_t layout(pif_ctx c, char* base) {
   c->idB = (int*)take(n * sizeof(int));
   c->key = (int*)take(n * sizeof(int));
   c->rnk = (int*)take(n * sizeof(int));
+  c->perm = (int*)take(n * sizeof(int));
   c->counts = (int*)take(c->max_bins * sizeof(int));
   c->offsets = (int*)take((c->max_bins + 1) * sizeof(int));
   c->soff = (int*)take((c->max_bins + 1) * sizeof(int));
@@ -467,8 +468,13 @@ pif_status sort_particles(pif_ctx c, Plan& p) {
   CU(cudaMemsetAsync(c->counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(c->xA, n, n, p.g, c->key, c->rnk, c->counts, c->st));
   CU(launch_schedule(c->counts, sched_of(c, p), p.g, keys_per_brick(p.g), p.g.C, c->st));
+#ifdef PIF_SCATTER_SORT
   CU(launch_scatter_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->xB,
                            c->vB, c->idB, nullptr, c->st));
+#else
+  CU(launch_gather_sorted(c->xA, c->vA, c->idA, n, n, c->key, c->rnk, c->offsets, c->perm, c->xB,
+                          c->vB, c->idB, c->st));
+#endif
   std::swap(c->xA, c->xB);
   std::swap(c->vA, c->vB);
   std::swap(c->idA, c->idB);
@@ -509,7 +515,9 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
     PH(PH_INTERP_PUSH, CU(launch_interp_push(p.grid3, c->xA, c->vA, n, c->idA, nullptr,
                                              sched_of(c, p), p.g, p.hc, P, c->st)));
-    c->launches += 7;  // bin, scan, scatter, spread, extract, poisson, interp_push
+    // own kernels: bin, schedule (reduce, partials, apply, fill), sort (index
+    // scatter + gather), spread, extract, poisson, interp_push (cuFFT not counted)
+    c->launches += 11;
     c->box_fresh = (which == 0) && !drift;
   } else {
     const int Ng = p.n;

@@ -183,6 +183,9 @@ cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* i
                                   int64_t stride, int64_t n, const int* key, const int* rank,
                                   const int* offsets, double* x2, double* v2, int* id2, double* s2,
                                   cudaStream_t st);
+cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id, int64_t stride,
+                                 int64_t n, const int* key, const int* rank, const int* offsets,
+                                 int* perm, double* x2, double* v2, int* id2, cudaStream_t st);
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
                           const Sched& S, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st);

@@ -246,6 +246,33 @@ __global__ void k_scatter_sorted(const double* __restrict__ x, const double* __r
   if (s) s2[dst] = s[j];
 }
 
+// Gather variant of the physical sort: perm[dst] = src (a 4-byte scatter),
+// then every array is gathered in destination order -- coalesced writes, and the
+// reads stay near-sequential because particles move less than a cell per step
+// (the partial-sector writes of a 52-byte-per-particle scatter are avoided).
+__global__ void k_scatter_index(int64_t n, const int* __restrict__ key,
+                                const int* __restrict__ rank, const int* __restrict__ offsets,
+                                int* __restrict__ perm) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  perm[offsets[key[j]] + rank[j]] = (int)j;
+}
+
+__global__ void k_gather_sorted(const double* __restrict__ x, const double* __restrict__ v,
+                                const int* __restrict__ id, int64_t stride, int64_t n,
+                                const int* __restrict__ perm, double* __restrict__ x2,
+                                double* __restrict__ v2, int* __restrict__ id2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = perm[i];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    x2[d * stride + i] = x[d * stride + j];
+    v2[d * stride + i] = v[d * stride + j];
+  }
+  id2[i] = id[j];
+}
+
 __global__ void k_iota(int* id, int64_t n) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < n) id[j] = (int)j;
@@ -288,6 +315,15 @@ cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* i
   if (n > 0)
     k_scatter_sorted<<<nblk(n, 256), 256, 0, st>>>(x, v, id, s, stride, n, key, rank, offsets, x2,
                                                    v2, id2, s2);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id, int64_t stride,
+                                 int64_t n, const int* key, const int* rank, const int* offsets,
+                                 int* perm, double* x2, double* v2, int* id2, cudaStream_t st) {
+  if (n > 0) {
+    k_scatter_index<<<nblk(n, 256), 256, 0, st>>>(n, key, rank, offsets, perm);
+    k_gather_sorted<<<nblk(n, 256), 256, 0, st>>>(x, v, id, stride, n, perm, x2, v2, id2);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_iota(int* id, int64_t n, cudaStream_t st) {
