@@ -26,7 +26,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 SHORT = {"k_interp_push": "interp_push", "k_spread": "spread", "k_bin_count": "bin_count",
-         "k_scatter_sorted": "scatter_sorted"}
+         "k_scatter_sorted": "scatter_sorted", "k_scatter_index": "scatter_index",
+         "k_gather_sorted": "gather_sorted"}
 
 
 def launches(path):
