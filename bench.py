@@ -281,7 +281,7 @@ def run_ours(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_sample = (1 << 17) * 32 ** 3 // N_MODES ** 3  # ~10-30 s of NUDFT work
+        n_sample = (3 << 17) * 32 ** 3 // N_MODES ** 3  # ~14 s of NUDFT work on 16 host cores (4.7 s per 2^17)
         rate, secs, threads = oracle_step_rate(n_sample, seed=CFG)
         cpu = {"value": rate, "unit": "particles/s", "cores": threads, "kind": "oracle",
                "sample": f"{n_sample} of the {N_PER_GPU} configs[{CFG}] {CASE} particles, one KDK "
