@@ -25,10 +25,16 @@
  * N/2-1.
  *
  * Ownership: every pointer passed in is BORROWED -- the library never frees it.
- * Device memory used by a context is one caller-allocated workspace
+ * Device memory used by pif_step is one caller-allocated workspace
  * (pif_workspace_size / pif_set_workspace; the Python binding allocates it as
- * a torch uint8 tensor).  The context handle is library-owned
- * (pif_finalize releases it).
+ * a torch uint8 tensor).  Two calls allocate temporaries outside it, stream-
+ * ordered (cudaMallocAsync) and released before they return, on every exit
+ * path: pif_parareal holds its parareal states there -- (2 n_slices + 4)
+ * states of (6 n_local + 1) doubles with time_size == 1, 5 states per time
+ * rank otherwise -- and the debug exports their input / sort buffers.  The
+ * context handle is library-owned (pif_finalize releases it).  Every call runs
+ * on the context's device (pif_dist.device) and restores the caller's current
+ * device before returning.
  *
  * Streams: all device work is ordered on pif_dist.stream (a cudaStream_t,
  * NULL = legacy default stream).  pif_step is asynchronous; pif_set_state /
@@ -59,7 +65,10 @@ typedef enum {
   PIF_ERR_NUMERIC = 3, /* non-finite value detected: checked by pif_set_state (input),
                           pif_get_state, pif_field_energy and each parareal correction */
   PIF_ERR_CUDA = 4,    /* CUDA runtime / cuFFT error (message has the code) */
-  PIF_ERR_NCCL = 5,    /* NCCL error */
+  PIF_ERR_NCCL = 5,    /* NCCL error, asynchronous NCCL error, or the watchdog: a synchronising
+                          call saw no progress for PIF_NCCL_TIMEOUT_S seconds (environment,
+                          default 600; a lost peer).  The communicators are then aborted and
+                          the context only accepts pif_finalize. */
   PIF_ERR_OOM = 6,     /* workspace too small */
   PIF_ERR_STATE = 7    /* call out of order (e.g. step before set_state / set_workspace) */
 } pif_status;
@@ -127,8 +136,10 @@ pif_status pif_workspace_size(pif_ctx ctx, size_t* bytes);
 pif_status pif_set_workspace(pif_ctx ctx, void* dptr, size_t bytes);
 
 /* Copy the local state in ([3][n_local] SoA each).  on_device = 1: CUDA
-   pointers; 0: host pointers (pinned or pageable).  Resets the time level.
-   Synchronises; PIF_ERR_NUMERIC (and no state) if any value is non-finite. */
+   pointers; 0: host pointers (pinned or pageable).  Positions outside the
+   periodic box are wrapped into [0, L)^3 (x - L floor(x / L)), so any finite
+   input is legal.  Resets the time level.  Synchronises; PIF_ERR_NUMERIC (and
+   no state) if any value is non-finite. */
 pif_status pif_set_state(pif_ctx ctx, const double* x, const double* v, int64_t n_local,
                          int on_device);
 /* Copy the local state out at an integer time level, in the ORIGINAL particle

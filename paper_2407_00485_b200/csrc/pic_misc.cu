@@ -143,10 +143,15 @@ __global__ void __launch_bounds__(256) k_reduce4(const double* __restrict__ part
   block_sum4_m(a, out4);
 }
 
-__global__ void k_check_finite(const double* __restrict__ a, int64_t count, int* flag) {
+// flag <- 1 if any a[i] is non-finite; L > 0: also wrap a[i] into [0, L) in
+// place (positions given outside the periodic box, any number of periods).
+__global__ void k_check_finite(double* __restrict__ a, int64_t count, double L, int* flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(a[i])) atomicExch(flag, 1);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double y = a[i];
+    if (!isfinite(y)) atomicExch(flag, 1);
+    else if (L > 0.0 && !(y >= 0.0 && y < L)) a[i] = wrapL(y, L);
+  }
 }
 
 // fp64 <-> fp32 staging for the fp32 density all-reduce (PIF_FLAG_FP32_ALLREDUCE)
@@ -188,8 +193,8 @@ cudaError_t launch_correct_norms(const double* F, const double* Gn, const double
   k_reduce4<<<1, 256, 0, st>>>(partials, kReduceBlocks, out4);
   return cudaGetLastError();
 }
-cudaError_t launch_check_finite(const double* a, int64_t count, int* flag, cudaStream_t st) {
-  k_check_finite<<<kReduceBlocks, 256, 0, st>>>(a, count, flag);
+cudaError_t launch_check_finite(double* a, int64_t count, double wrap_L, int* flag, cudaStream_t st) {
+  k_check_finite<<<kReduceBlocks, 256, 0, st>>>(a, count, wrap_L, flag);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,8 @@
 #include <functional>
 #include <cmath>
 #include <string>
+#include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "pif_internal.cuh"
@@ -49,6 +51,40 @@ pif_status fail(pif_status s, const std::string& msg) {
     pif_status s_ = (call);       \
     if (s_ != PIF_OK) return s_;  \
   } while (0)
+
+// Every entry point that touches device state runs on the context's device and
+// restores the caller's current device on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Temporary device buffers outside the workspace (debug exports, parareal
+// states): stream-ordered allocations freed on every exit path.
+struct DevBufs {
+  cudaStream_t st;
+  std::vector<void*> v;
+  explicit DevBufs(cudaStream_t s) : st(s) {}
+  template <typename T>
+  cudaError_t alloc(T** p, size_t bytes) {
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, bytes, st);
+    if (e != cudaSuccess) return e;
+    v.push_back(q);
+    *p = static_cast<T*>(q);
+    return cudaSuccess;
+  }
+  ~DevBufs() {
+    for (void* q : v) cudaFreeAsync(q, st);
+    if (!v.empty()) cudaStreamSynchronize(st);
+  }
+};
 
 // ---------------------------------------------------------------------------
 // NUFFT parameters (reading R12): w = ceil(-log10(eps/10)), beta = c(w) w, n =
@@ -196,6 +232,7 @@ struct pif_ctx_s {
   ncclComm_t comm_tp[2] = {nullptr, nullptr};
   cudaStream_t st_comm = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_sent = nullptr;
+  bool nccl_broken = false;  // communicators aborted (async error / timeout)
   // workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -220,63 +257,70 @@ struct pif_ctx_s {
 
 namespace {
 
-// Walk the workspace layout (256-byte aligned buffers); base == nullptr: size only.
+// Walk the workspace layout (256-byte aligned buffers).  base == nullptr: size
+// only, the context is not touched (so a size query or a failed
+// pif_set_workspace never clobbers live buffer pointers); otherwise the
+// context's buffer pointers are assigned from base.
 size_t layout(pif_ctx c, char* base) {
+  const bool assign = base != nullptr;
   size_t off = 0;
-  auto take = [&](size_t bytes) -> char* {
+  auto take = [&](auto& dst, size_t bytes) {
     off = (off + 255) & ~(size_t)255;
-    char* p = base ? base + off : nullptr;
+    if (assign) dst = reinterpret_cast<std::remove_reference_t<decltype(dst)>>(base + off);
     off += bytes;
-    return p;
   };
   const int64_t n = std::max<int64_t>(c->nloc, 1);
-  c->xA = (double*)take(3 * n * sizeof(double));
-  c->vA = (double*)take(3 * n * sizeof(double));
-  c->xB = (double*)take(3 * n * sizeof(double));
-  c->vB = (double*)take(3 * n * sizeof(double));
-  c->idA = (int*)take(n * sizeof(int));
-  c->idB = (int*)take(n * sizeof(int));
-  c->key = (int*)take(n * sizeof(int));
-  c->rnk = (int*)take(n * sizeof(int));
-  c->perm = (int*)take(n * sizeof(int));
-  c->counts = (int*)take(c->max_bins * sizeof(int));
-  c->offsets = (int*)take((c->max_bins + 1) * sizeof(int));
-  c->soff = (int*)take((c->max_bins + 1) * sizeof(int));
-  c->ioff = (int*)take((c->max_bins + 1) * sizeof(int));
-  c->moff = (int*)take((c->max_bins + 1) * sizeof(int));
-  c->spart = (int*)take(sched_part_ints(c->max_bins) * sizeof(int));
-  c->max_s = c->max_i = 1;
+  take(c->xA, 3 * n * sizeof(double));
+  take(c->vA, 3 * n * sizeof(double));
+  take(c->xB, 3 * n * sizeof(double));
+  take(c->vB, 3 * n * sizeof(double));
+  take(c->idA, n * sizeof(int));
+  take(c->idB, n * sizeof(int));
+  take(c->key, n * sizeof(int));
+  take(c->rnk, n * sizeof(int));
+  take(c->perm, n * sizeof(int));
+  take(c->counts, c->max_bins * sizeof(int));
+  take(c->offsets, (c->max_bins + 1) * sizeof(int));
+  take(c->soff, (c->max_bins + 1) * sizeof(int));
+  take(c->ioff, (c->max_bins + 1) * sizeof(int));
+  take(c->moff, (c->max_bins + 1) * sizeof(int));
+  take(c->spart, sched_part_ints(c->max_bins) * sizeof(int));
+  int64_t max_s = 1, max_i = 1;
   for (int i = 0; i < 2; ++i) {
     const Plan& p = c->plan[i];
     if (!p.valid || p.kind != PIF_PROP_PIF_NUFFT) continue;
     const int64_t M = keys_per_brick(p.g);
-    c->max_s = std::max(c->max_s, sched_max_s(p.nbricks, M, n));
-    c->max_i = std::max(c->max_i, sched_max_i(p.nbricks, n));
+    max_s = std::max(max_s, sched_max_s(p.nbricks, M, n));
+    max_i = std::max(max_i, sched_max_i(p.nbricks, n));
   }
-  c->sitems = (int4*)take(c->max_s * sizeof(int4));
-  c->iitems = (int4*)take(c->max_i * sizeof(int4));
-  c->iinfo = (int4*)take(c->max_i * sizeof(int4));
-  c->flag = (int*)take(64);
-  c->partials = (double*)take(4 * kReduceBlocks * sizeof(double));
-  c->red = (double*)take(16 * sizeof(double));
+  if (assign) {
+    c->max_s = max_s;
+    c->max_i = max_i;
+  }
+  take(c->sitems, max_s * sizeof(int4));
+  take(c->iitems, max_i * sizeof(int4));
+  take(c->iinfo, max_i * sizeof(int4));
+  take(c->flag, 64);
+  take(c->partials, 4 * kReduceBlocks * sizeof(double));
+  take(c->red, 16 * sizeof(double));
   size_t fw = 0;
   for (int i = 0; i < 2; ++i) {
     Plan& p = c->plan[i];
     if (!p.valid) continue;
     fw = std::max(fw, std::max(p.wfwd, p.winv));
-    p.grid = (double*)take(p.grid_pts() * sizeof(double));
-    p.spec = (double2*)take(p.spec_elems() * sizeof(double2));
-    p.G3 = (double2*)take(3 * p.spec_elems() * sizeof(double2));
-    p.grid3 = (double*)take(3 * p.grid_pts() * sizeof(double));
+    take(p.grid, p.grid_pts() * sizeof(double));
+    take(p.spec, p.spec_elems() * sizeof(double2));
+    take(p.G3, 3 * p.spec_elems() * sizeof(double2));
+    take(p.grid3, 3 * p.grid_pts() * sizeof(double));
     if (p.fp32_ar)
-      p.ar32 = take((p.kind == PIF_PROP_PIF_NUFFT ? 2 * p.box_elems() : p.grid_pts()) * sizeof(float));
+      take(p.ar32, (p.kind == PIF_PROP_PIF_NUFFT ? 2 * p.box_elems() : p.grid_pts()) * sizeof(float));
     if (p.kind == PIF_PROP_PIF_NUFFT) {
-      p.box = (double2*)take(p.box_elems() * sizeof(double2));
-      p.cor = (double*)take((p.N + 1) * sizeof(double));
-      p.S = (double*)take((p.N + 1) * sizeof(double));
+      take(p.box, p.box_elems() * sizeof(double2));
+      take(p.cor, (p.N + 1) * sizeof(double));
+      take(p.S, (p.N + 1) * sizeof(double));
     }
   }
-  c->fft_work = take(std::max<size_t>(fw, 256));
+  take(c->fft_work, std::max<size_t>(fw, 256));
   return off + 256;
 }
 
@@ -315,12 +359,7 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     else if (w <= 5) { RI[0] = RI[1] = RI[2] = 8; }
     else if (w == 8 && ppc >= PIF_W8_PPC) { RI[0] = RI[1] = 10; RI[2] = 8; m[0] = m[1] = 3; }  // spread 16x16x8
     else if (w <= 9) { RI[0] = RI[1] = RI[2] = 12; }
-#ifndef PIF_W13_TILE
-#define PIF_W13_TILE 1
-#endif
-    else if (w == 13 && PIF_W13_TILE == 1) { RI[0] = 14; RI[1] = 14; RI[2] = 16; m[0] = m[1] = 2; }
-    else if (w == 13 && PIF_W13_TILE == 2) { RI[0] = 16; RI[1] = 14; RI[2] = 16; m[1] = 2; }
-    else if (w == 13 && PIF_W13_TILE == 3) { RI[0] = RI[1] = RI[2] = 16; }
+    else if (w == 13) { RI[0] = 14; RI[1] = 14; RI[2] = 16; m[0] = m[1] = 2; }
     else { RI[0] = RI[1] = RI[2] = 16; }
     Brick& g = p.g;
     g.n = n;
@@ -468,13 +507,8 @@ pif_status sort_particles(pif_ctx c, Plan& p) {
   CU(cudaMemsetAsync(c->counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(c->xA, n, n, p.g, c->key, c->rnk, c->counts, c->st));
   CU(launch_schedule(c->counts, sched_of(c, p), p.g, keys_per_brick(p.g), p.g.C, c->st));
-#ifdef PIF_SCATTER_SORT
-  CU(launch_scatter_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->xB,
-                           c->vB, c->idB, nullptr, c->st));
-#else
-  CU(launch_gather_sorted(c->xA, c->vA, c->idA, n, n, c->key, c->rnk, c->offsets, c->perm, c->xB,
-                          c->vB, c->idB, c->st));
-#endif
+  CU(launch_gather_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->perm,
+                          c->xB, c->vB, c->idB, nullptr, c->st));
   std::swap(c->xA, c->xB);
   std::swap(c->vA, c->vB);
   std::swap(c->idA, c->idB);
@@ -562,12 +596,72 @@ pif_status step_internal(pif_ctx c, int which, int64_t nsteps) {
   return PIF_OK;
 }
 
-// PIF_ERR_NUMERIC check: any non-finite value in a[0..count) (synchronises).
-pif_status check_finite(pif_ctx c, const double* a, int64_t count, const char* what) {
+// Failure detection for the multi-process paths: abort every communicator of
+// the context (pending NCCL kernels then return), after which the context only
+// accepts pif_finalize.
+void abort_comms(pif_ctx c) {
+  ncclComm_t* all[] = {&c->comm_tp[0], &c->comm_tp[1], &c->comm_space, &c->comm_time, &c->comm_world};
+  for (ncclComm_t* p : all)
+    if (*p) {
+      ncclCommAbort(*p);
+      *p = nullptr;
+    }
+  c->nccl_broken = true;
+}
+
+double nccl_timeout_s() {
+  const char* e = getenv("PIF_NCCL_TIMEOUT_S");
+  const double t = e ? atof(e) : 0.0;
+  return t > 0 ? t : 600.0;
+}
+
+// Wait for stream st.  world == 1: cudaStreamSynchronize.  Otherwise poll the
+// stream and every communicator's asynchronous error state, so that an NCCL
+// error or a peer that never answers (no progress for PIF_NCCL_TIMEOUT_S
+// seconds, default 600) aborts the communicators and returns PIF_ERR_NCCL
+// instead of hanging every later slice of the parareal pipeline.
+pif_status sync_stream(pif_ctx c, cudaStream_t st) {
+  if (c->world == 1) {
+    CU(cudaStreamSynchronize(st));
+    return PIF_OK;
+  }
+  if (c->nccl_broken) return fail(PIF_ERR_NCCL, "communicators were aborted by an earlier NCCL failure");
+  const double t0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  const double limit = nccl_timeout_s();
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return PIF_OK;
+    if (e != cudaErrorNotReady) return fail(PIF_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+    if ((spin & 255) != 255) continue;
+    ncclComm_t comms[] = {c->comm_world, c->comm_space, c->comm_time, c->comm_tp[0], c->comm_tp[1]};
+    for (ncclComm_t cm : comms) {
+      if (!cm) continue;
+      ncclResult_t ae = ncclSuccess;
+      if (ncclCommGetAsyncError(cm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+        abort_comms(c);
+        return fail(PIF_ERR_NCCL, std::string("asynchronous NCCL error: ") + ncclGetErrorString(ae));
+      }
+    }
+    const double t = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (t - t0 > limit) {
+      abort_comms(c);
+      return fail(PIF_ERR_NCCL, "NCCL watchdog: no progress for " + std::to_string(limit) +
+                                    " s (lost peer?); communicators aborted");
+    }
+    std::this_thread::yield();
+  }
+}
+
+// PIF_ERR_NUMERIC check of (a, na) and (b, nb) (b may be null) with one
+// synchronisation.  wrap_L > 0: a holds positions, wrapped into [0, L) in place
+// (inputs outside the periodic box are legal; anchor_of needs [0, L)).
+pif_status check_state(pif_ctx c, double* a, int64_t na, const double* b, int64_t nb, double wrap_L,
+                       const char* what) {
   CU(cudaMemsetAsync(c->flag, 0, sizeof(int), c->st));
-  CU(launch_check_finite(a, count, c->flag, c->st));
+  CU(launch_check_finite(a, na, wrap_L, c->flag, c->st));
+  if (b) CU(launch_check_finite(const_cast<double*>(b), nb, 0.0, c->flag, c->st));
   CU(cudaMemcpyAsync(&c->host_red[12], c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  CU(cudaStreamSynchronize(c->st));
+  TRY(sync_stream(c, c->st));
   int bad = 0;
   memcpy(&bad, &c->host_red[12], sizeof(int));
   if (bad) return fail(PIF_ERR_NUMERIC, std::string("non-finite values in ") + what);
@@ -661,11 +755,14 @@ pif_status pif_init(const pif_physics* phys, const pif_propagator* fine,
     g_err = msg;
     return s;
   };
-  cudaError_t e = cudaSetDevice(c->device);
-  if (e != cudaSuccess) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || c->device < 0 || c->device >= ndev) {
     delete c;
-    return fail(PIF_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    return fail(PIF_ERR_CUDA, std::string("no CUDA device ") + std::to_string(dist->device) + ": " +
+                                  cudaGetErrorString(e));
   }
+  DeviceGuard dg(c->device);
   pif_status s = make_plan(c, 0, fine);
   if (s != PIF_OK) return bail(s);
   if (coarse) {
@@ -758,6 +855,8 @@ pif_status pif_set_workspace(pif_ctx c, void* dptr, size_t bytes) {
   if ((uintptr_t)dptr % 256) return fail(PIF_ERR_ARG, "workspace must be 256-byte aligned");
   size_t need = layout(c, nullptr);
   if (bytes < need) return fail(PIF_ERR_OOM, "workspace too small: need " + std::to_string(need));
+  DeviceGuard dg(c->device);
+  TRY(sync_stream(c, c->st));  // nothing in flight may use the old workspace
   layout(c, (char*)dptr);
   c->ws = dptr;
   c->ws_bytes = bytes;
@@ -771,7 +870,7 @@ pif_status pif_set_workspace(pif_ctx c, void* dptr, size_t bytes) {
       CU(cudaMemcpyAsync(p.S, p.hS.data(), (p.N + 1) * sizeof(double), cudaMemcpyHostToDevice, c->st));
     }
   }
-  CU(cudaStreamSynchronize(c->st));
+  TRY(sync_stream(c, c->st));
   c->has_state = false;
   return PIF_OK;
 }
@@ -781,14 +880,14 @@ pif_status pif_set_state(pif_ctx c, const double* x, const double* v, int64_t n_
   if (!c || !x || !v) return fail(PIF_ERR_ARG, "null argument");
   if (!c->ws) return fail(PIF_ERR_STATE, "workspace not set");
   if (n_local != c->nloc) return fail(PIF_ERR_ARG, "n_local mismatch: expected " + std::to_string(c->nloc));
+  DeviceGuard dg(c->device);
   const size_t b = 3 * n_local * sizeof(double);
   cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   CU(cudaMemcpyAsync(c->xA, x, b, k, c->st));
   CU(cudaMemcpyAsync(c->vA, v, b, k, c->st));
   CU(launch_iota(c->idA, n_local, c->st));
   c->has_state = false;
-  TRY(check_finite(c, c->xA, 3 * n_local, "the input positions"));
-  TRY(check_finite(c, c->vA, 3 * n_local, "the input velocities"));
+  TRY(check_state(c, c->xA, 3 * n_local, c->vA, 3 * n_local, c->ph.L, "the input state"));
   c->has_state = true;
   c->pending = false;
   c->box_fresh = false;
@@ -799,15 +898,15 @@ pif_status pif_get_state(pif_ctx c, double* x, double* v, int64_t n_local, int o
   TRY(need_ready(c));
   if (!x || !v) return fail(PIF_ERR_ARG, "null argument");
   if (n_local != c->nloc) return fail(PIF_ERR_ARG, "n_local mismatch");
+  DeviceGuard dg(c->device);
   TRY(materialize(c));
   const int64_t n = c->nloc;
   CU(launch_scatter_by_id(c->xA, c->vA, c->idA, n, n, c->xB, c->vB, c->st));
-  TRY(check_finite(c, c->xB, 3 * n, "the positions"));
-  TRY(check_finite(c, c->vB, 3 * n, "the velocities"));
+  TRY(check_state(c, c->xB, 3 * n, c->vB, 3 * n, 0.0, "the state"));
   cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   CU(cudaMemcpyAsync(x, c->xB, 3 * n * sizeof(double), k, c->st));
   CU(cudaMemcpyAsync(v, c->vB, 3 * n * sizeof(double), k, c->st));
-  if (!on_device) CU(cudaStreamSynchronize(c->st));
+  if (!on_device) TRY(sync_stream(c, c->st));
   return PIF_OK;
 }
 
@@ -815,6 +914,8 @@ pif_status pif_step(pif_ctx c, int which, int64_t n_steps) {
   TRY(need_ready(c));
   if (which < 0 || which > 1 || !c->plan[which].valid) return fail(PIF_ERR_ARG, "no such propagator");
   if (n_steps < 0) return fail(PIF_ERR_ARG, "n_steps must be >= 0");
+  if (c->nccl_broken) return fail(PIF_ERR_NCCL, "communicators were aborted by an earlier NCCL failure");
+  DeviceGuard dg(c->device);
   return step_internal(c, which, n_steps);
 }
 
@@ -822,6 +923,7 @@ pif_status pif_field_energy(pif_ctx c, double W[3], double* kinetic, double mome
                             double* charge_err) {
   TRY(need_ready(c));
   if (!W || !kinetic || !momentum || !charge_err) return fail(PIF_ERR_ARG, "null argument");
+  DeviceGuard dg(c->device);
   TRY(materialize(c));
   Plan& p = c->plan[0];
   if (!c->box_fresh) TRY(solve_and_push(c, 0, 0, 0));
@@ -836,7 +938,7 @@ pif_status pif_field_energy(pif_ctx c, double W[3], double* kinetic, double mome
   if (c->space_size > 1)
     NC(ncclAllReduce(c->red + 4, c->red + 4, 4, ncclDouble, ncclSum, c->comm_space, c->st));
   CU(cudaMemcpyAsync(c->host_red, c->red, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  CU(cudaStreamSynchronize(c->st));
+  TRY(sync_stream(c, c->st));
   const double* r = c->host_red;
   if (p.kind == PIF_PROP_PIF_NUFFT) {
     for (int d = 0; d < 3; ++d) W[d] = r[d];
@@ -858,10 +960,11 @@ pif_status pif_get_rho(pif_ctx c, double* out) {
   if (!out) return fail(PIF_ERR_ARG, "null argument");
   Plan& p = c->plan[0];
   if (p.kind != PIF_PROP_PIF_NUFFT) return fail(PIF_ERR_CONFIG, "fine propagator is not PIF");
+  DeviceGuard dg(c->device);
   TRY(materialize(c));
   if (!c->box_fresh) TRY(solve_and_push(c, 0, 0, 0));
   CU(cudaMemcpyAsync(out, p.box, p.box_elems() * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
-  CU(cudaStreamSynchronize(c->st));
+  TRY(sync_stream(c, c->st));
   return PIF_OK;
 }
 
@@ -890,23 +993,20 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
   for (int i = 0; i < max_iter * n_slices; ++i) rep->err_x[i] = rep->err_v[i] = NAN;
   for (int i = 0; i < n_slices; ++i) rep->retired_at[i] = -1;
 
-  std::vector<double*> bufs;
+  // Parareal states live outside the workspace (include/pif.h): stream-ordered
+  // allocations released on every exit path.
+  DevBufs bufs(c->st);
   auto alloc = [&](double** p) -> pif_status {
-    CU(cudaMallocAsync((void**)p, SZ * sizeof(double), c->st));
+    CU(bufs.alloc(p, SZ * sizeof(double)));
     CU(cudaMemsetAsync(*p, 0, SZ * sizeof(double), c->st));
-    bufs.push_back(*p);
     return PIF_OK;
   };
-  auto free_all = [&]() {
-    for (double* b : bufs) cudaFreeAsync(b, c->st);
-    cudaStreamSynchronize(c->st);
-  };
   auto timed = [&](double& acc, auto fn) -> pif_status {
-    CU(cudaStreamSynchronize(c->st));
+    TRY(sync_stream(c, c->st));
     double a = now();
     pif_status s = fn();
     if (s != PIF_OK) return s;
-    CU(cudaStreamSynchronize(c->st));
+    TRY(sync_stream(c, c->st));
     acc += now() - a;
     return PIF_OK;
   };
@@ -923,7 +1023,7 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
     CU(launch_correct_norms(F, Gn, Go, U, n, L, c->partials, c->red, c->st));
     if (c->space_size > 1) NC(ncclAllReduce(c->red, c->red, 4, ncclDouble, ncclSum, c->comm_space, c->st));
     CU(cudaMemcpyAsync(c->host_red, c->red, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CU(cudaStreamSynchronize(c->st));
+    TRY(sync_stream(c, c->st));
     const double* r = c->host_red;
     ex = r[1] > 0 ? std::sqrt(r[0] / r[1]) : std::sqrt(r[0]);
     ev = r[3] > 0 ? std::sqrt(r[2] / r[3]) : std::sqrt(r[2]);
@@ -938,9 +1038,9 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
     // ---------------- reference schedule: all slices on this rank ----------
     std::vector<double*> U(n_slices + 1), Gold(n_slices);
     double *Fcur, *Fnext, *Gnew;
-    for (auto& p : U) if ((st = alloc(&p)) != PIF_OK) { free_all(); return st; }
-    for (auto& p : Gold) if ((st = alloc(&p)) != PIF_OK) { free_all(); return st; }
-    if ((st = alloc(&Fcur)) || (st = alloc(&Fnext)) || (st = alloc(&Gnew))) { free_all(); return st; }
+    for (auto& p : U) if ((st = alloc(&p)) != PIF_OK) return st;
+    for (auto& p : Gold) if ((st = alloc(&p)) != PIF_OK) return st;
+    if ((st = alloc(&Fcur)) || (st = alloc(&Fnext)) || (st = alloc(&Gnew))) return st;
     std::vector<char> changed(n_slices, 1), retired(n_slices, 0);
     st = store_state(c, U[0]);
     // iteration 0: serial coarse sweep
@@ -994,7 +1094,7 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
     const int t = c->t_idx, T = c->time_size;
     double* buf[5];
     for (auto& p : buf)
-      if ((st = alloc(&p)) != PIF_OK) { free_all(); return st; }
+      if ((st = alloc(&p)) != PIF_OK) return st;
     struct GpuOps {
       pif_ctx c;
       double** buf;
@@ -1044,7 +1144,7 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
         NC(ncclRecv(g->buf[b], g->SZ, ncclDouble, g->t - 1, c->comm_tp[(g->t + 1) % 2], c->st));
         CU(cudaMemcpyAsync(&c->host_red[8], g->buf[b] + 6 * g->n, sizeof(double),
                            cudaMemcpyDeviceToHost, c->st));
-        CU(cudaStreamSynchronize(c->st));
+        TRY(sync_stream(c, c->st));
         *flag = c->host_red[8];
         return PIF_OK;
       });
@@ -1061,13 +1161,16 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
     std::vector<double>& myx = pr.ex;
     std::vector<double>& myv = pr.ev;
     int my_ret = pr.retired_at;
-    if (c->st_comm) cudaStreamSynchronize(c->st_comm);
+    if (c->st_comm) {
+      pif_status s2 = sync_stream(c, c->st_comm);
+      if (st == PIF_OK) st = s2;
+    }
     if (st == PIF_OK) st = load_state(c, Unext);
     // gather the report over the time group (small)
     if (st == PIF_OK && max_iter > 0) {
       double* d = nullptr;
       const int64_t rowsz = 2 * (int64_t)max_iter + 2;
-      CU(cudaMallocAsync((void**)&d, rowsz * (T + 1) * sizeof(double), c->st));
+      CU(bufs.alloc(&d, rowsz * (T + 1) * sizeof(double)));
       std::vector<double> row(rowsz);
       for (int k = 0; k < max_iter; ++k) {
         row[k] = myx[k];
@@ -1079,8 +1182,7 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
       NC(ncclAllGather(d, d + rowsz, rowsz, ncclDouble, c->comm_time, c->st));
       std::vector<double> all(rowsz * T);
       CU(cudaMemcpyAsync(all.data(), d + rowsz, rowsz * T * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-      CU(cudaStreamSynchronize(c->st));
-      cudaFreeAsync(d, c->st);
+      TRY(sync_stream(c, c->st));
       int conv = 1;
       iterations = 0;
       for (int s = 0; s < T; ++s) {
@@ -1096,7 +1198,6 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
       rep->converged = conv;
     }
   }
-  free_all();
   if (st != PIF_OK) return st;
   rep->iterations = iterations;
   rep->t_coarse0 = t_coarse0;
@@ -1116,6 +1217,7 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
     return fail(PIF_ERR_ARG, "bad slices / iterations / interval / blocks");
   if (c->time_size > 1 && n_slices != c->time_size)
     return fail(PIF_ERR_CONFIG, "n_slices must equal the number of time ranks");
+  DeviceGuard dg(c->device);
   // Multi-block parareal (reading R22): n_blocks equal windows solved
   // one after the other, each by parareal with n_slices slices; the final state
   // of a window (on the last time rank) seeds the next window on every rank.
@@ -1136,13 +1238,13 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
       // hand U_{n_slices} of this window from the last time rank to all time ranks
       double t0c = now();
       const int64_t n = c->nloc;
+      DevBufs hb(c->st);
       double* buf = nullptr;
-      CU(cudaMallocAsync((void**)&buf, 6 * n * sizeof(double), c->st));
+      CU(hb.alloc(&buf, 6 * n * sizeof(double)));
       if (c->t_idx == c->time_size - 1) TRY(store_state(c, buf));
       NC(ncclBroadcast(buf, buf, 6 * n, ncclDouble, c->time_size - 1, c->comm_time, c->st));
       TRY(load_state(c, buf));
-      CU(cudaFreeAsync(buf, c->st));
-      CU(cudaStreamSynchronize(c->st));
+      TRY(sync_stream(c, c->st));
       tc += now() - t0c;
       tt += now() - t0c;
     }
@@ -1167,7 +1269,8 @@ pif_status pif_profile_read(pif_ctx c, double* phase_ms, int32_t n_phases, int64
                             int reset) {
   if (!c || !phase_ms || !launches || n_phases < PIF_NPHASES)
     return fail(PIF_ERR_ARG, "need phase_ms[PIF_NPHASES] and launches");
-  CU(cudaStreamSynchronize(c->st));
+  DeviceGuard dg(c->device);
+  TRY(sync_stream(c, c->st));
   for (int ph = 0; ph < PIF_NPHASES; ++ph) {
     double acc = 0;
     for (size_t i = 0; i + 1 < c->ev_used[ph]; i += 2) {
@@ -1186,6 +1289,7 @@ pif_status pif_profile_read(pif_ctx c, double* phase_ms, int32_t n_phases, int64
 
 pif_status pif_finalize(pif_ctx c) {
   if (!c) return PIF_OK;
+  DeviceGuard dg(c->device);
   for (int ph = 0; ph < PIF_NPHASES; ++ph)
     for (cudaEvent_t e : c->ev[ph]) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -1206,96 +1310,98 @@ pif_status pif_finalize(pif_ctx c) {
 }
 
 // ------------------------------------------------------------- debug/tests --
-// Temporary schedule for the debug transforms (one cudaMalloc: counts + Sched).
-static pif_status debug_sched(pif_ctx c, const Plan& p, int64_t n, int** counts, Sched& S) {
+// Device buffers of a debug transform on n particles: positions (and
+// strengths) in caller order, their sorted copies, and the sort / schedule
+// arrays of plan p -- the production bin, schedule and gather sort.
+struct DebugSort {
+  double *x = nullptr, *x2 = nullptr, *s = nullptr, *s2 = nullptr;
+  int *id = nullptr, *id2 = nullptr, *key = nullptr, *rk = nullptr, *perm = nullptr, *counts = nullptr;
+  Sched S{};
+};
+static pif_status debug_sort(pif_ctx c, const Plan& p, DevBufs& B, const double* x, const double* s,
+                             int64_t n, DebugSort& D) {
   const int64_t K = p.nbricks, M = keys_per_brick(p.g);
   const int64_t ms = sched_max_s(K, M, n), mi = sched_max_i(K, n);
-  const size_t ints = K + 4 * (K + 1) + sched_part_ints(K);
-  char* buf = nullptr;
-  CU(cudaMalloc(&buf, ints * sizeof(int) + 16 + (ms + 2 * mi) * sizeof(int4)));
-  int* ib = (int*)buf;
-  *counts = ib;
-  int4* items = (int4*)(((uintptr_t)(ib + ints) + 15) & ~(uintptr_t)15);
-  S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, ib + 4 * K + 3, items, items + ms, items + ms + mi,
-            ib + 5 * K + 4, K, ms, mi};
+  CU(B.alloc(&D.x, 3 * n * sizeof(double)));
+  CU(B.alloc(&D.x2, 3 * n * sizeof(double)));
+  if (s) {
+    CU(B.alloc(&D.s, n * sizeof(double)));
+    CU(B.alloc(&D.s2, n * sizeof(double)));
+  }
+  CU(B.alloc(&D.id, 5 * n * sizeof(int)));
+  D.id2 = D.id + n;
+  D.key = D.id + 2 * n;
+  D.rk = D.id + 3 * n;
+  D.perm = D.id + 4 * n;
+  int* ib = nullptr;
+  const size_t ints = K + 5 * (K + 1) + sched_part_ints(K);
+  CU(B.alloc(&ib, ints * sizeof(int)));
+  int4* items = nullptr;
+  CU(B.alloc(&items, (ms + 2 * mi) * sizeof(int4)));
+  D.counts = ib;
+  D.S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, ib + 4 * K + 3, items, items + ms, items + ms + mi,
+              ib + 5 * K + 5, K, ms, mi};
+  CU(cudaMemcpyAsync(D.x, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  if (s) CU(cudaMemcpyAsync(D.s, s, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CU(launch_iota(D.id, n, c->st));
+  CU(cudaMemsetAsync(D.counts, 0, K * sizeof(int), c->st));
+  CU(launch_bin_count(D.x, n, n, p.g, D.key, D.rk, D.counts, c->st));
+  CU(launch_schedule(D.counts, D.S, p.g, (int)M, p.g.C, c->st));
+  CU(launch_gather_sorted(D.x, nullptr, D.id, D.s, n, n, D.key, D.rk, D.S.offsets, D.perm, D.x2,
+                          nullptr, D.id2, D.s2, c->st));
   return PIF_OK;
 }
-pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, const double* s,
-                           double* out) {
-  if (!c || !x || !s || !out || n < 1) return fail(PIF_ERR_ARG, "null argument / empty input");
+
+static pif_status debug_args(pif_ctx c, int which, int64_t n) {
+  if (!c || n < 1) return fail(PIF_ERR_ARG, "null argument / empty input");
   if (!c->ws) return fail(PIF_ERR_STATE, "workspace not set");
   if (which < 0 || which > 1 || !c->plan[which].valid || c->plan[which].kind != PIF_PROP_PIF_NUFFT)
     return fail(PIF_ERR_ARG, "not a PIF propagator");
+  return PIF_OK;
+}
+
+pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, const double* s,
+                           double* out) {
+  TRY(debug_args(c, which, n));
+  if (!x || !s || !out) return fail(PIF_ERR_ARG, "null argument");
+  DeviceGuard dg(c->device);
   Plan& p = c->plan[which];
-  double *dx, *dx2, *ds, *ds2;
-  int *id, *id2, *key, *rk, *counts, *offs;
-  double2* dout;
   const int64_t N3 = (int64_t)p.N * p.N * p.N;
-  CU(cudaMalloc(&dx, 3 * n * sizeof(double)));
-  CU(cudaMalloc(&dx2, 3 * n * sizeof(double)));
-  CU(cudaMalloc(&ds, n * sizeof(double)));
-  CU(cudaMalloc(&ds2, n * sizeof(double)));
-  CU(cudaMalloc(&id, 4 * n * sizeof(int)));
-  id2 = id + n;
-  key = id + 2 * n;
-  rk = id + 3 * n;
-  Sched S;
-  TRY(debug_sched(c, p, n, &counts, S));
-  offs = S.offsets;
-  CU(cudaMalloc(&dout, N3 * sizeof(double2)));
-  CU(cudaMemcpyAsync(dx, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
-  CU(cudaMemcpyAsync(ds, s, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
-  CU(launch_iota(id, n, c->st));
-  CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
-  CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_schedule(counts, S, p.g, keys_per_brick(p.g), p.g.C, c->st));
-  CU(launch_scatter_sorted(dx, nullptr, id, ds, n, n, key, rk, offs, dx2, nullptr, id2, ds2, c->st));
+  DevBufs B(c->st);
+  DebugSort D;
+  TRY(debug_sort(c, p, B, x, s, n, D));
+  double2* dout = nullptr;
+  CU(B.alloc(&dout, N3 * sizeof(double2)));
   CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-  CU(launch_spread(dx2, n, ds2, 1.0, S, p.g, p.hc, p.grid, c->st));
+  CU(launch_spread(D.x2, n, D.s2, 1.0, D.S, p.g, p.hc, p.grid, c->st));
   CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec));
   CU(launch_debug_extract_KN(p.spec, p.n, p.N, p.cor, dout, c->st));
   CU(cudaMemcpyAsync(out, dout, N3 * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
-  CU(cudaStreamSynchronize(c->st));
-  cudaFree(dx); cudaFree(dx2); cudaFree(ds); cudaFree(ds2); cudaFree(id); cudaFree(counts); cudaFree(dout);
+  TRY(sync_stream(c, c->st));
   return PIF_OK;
 }
 
 pif_status pif_debug_type2(pif_ctx c, int which, const double* cin, const double* x, int64_t n,
                            double* out) {
-  if (!c || !x || !cin || !out || n < 1) return fail(PIF_ERR_ARG, "null argument / empty input");
-  if (!c->ws) return fail(PIF_ERR_STATE, "workspace not set");
-  if (which < 0 || which > 1 || !c->plan[which].valid || c->plan[which].kind != PIF_PROP_PIF_NUFFT)
-    return fail(PIF_ERR_ARG, "not a PIF propagator");
+  TRY(debug_args(c, which, n));
+  if (!x || !cin || !out) return fail(PIF_ERR_ARG, "null argument");
+  DeviceGuard dg(c->device);
   Plan& p = c->plan[which];
   const int64_t N3 = (int64_t)p.N * p.N * p.N;
-  double *dx, *dx2, *E;
-  int *id, *id2, *key, *rk, *counts, *offs;
-  double2* dc;
-  CU(cudaMalloc(&dx, 3 * n * sizeof(double)));
-  CU(cudaMalloc(&dx2, 3 * n * sizeof(double)));
-  CU(cudaMalloc(&E, 3 * n * sizeof(double)));
-  CU(cudaMalloc(&id, 4 * n * sizeof(int)));
-  id2 = id + n;
-  key = id + 2 * n;
-  rk = id + 3 * n;
-  Sched S;
-  TRY(debug_sched(c, p, n, &counts, S));
-  offs = S.offsets;
-  CU(cudaMalloc(&dc, N3 * sizeof(double2)));
-  CU(cudaMemcpyAsync(dx, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  DevBufs B(c->st);
+  DebugSort D;
+  TRY(debug_sort(c, p, B, x, nullptr, n, D));
+  double *E = nullptr;
+  double2* dc = nullptr;
+  CU(B.alloc(&E, 3 * n * sizeof(double)));
+  CU(B.alloc(&dc, N3 * sizeof(double2)));
   CU(cudaMemcpyAsync(dc, cin, N3 * sizeof(double2), cudaMemcpyHostToDevice, c->st));
-  CU(launch_iota(id, n, c->st));
-  CU(cudaMemsetAsync(counts, 0, p.nbricks * sizeof(int), c->st));
-  CU(launch_bin_count(dx, n, n, p.g, key, rk, counts, c->st));
-  CU(launch_schedule(counts, S, p.g, keys_per_brick(p.g), p.g.C, c->st));
-  CU(launch_scatter_sorted(dx, nullptr, id, nullptr, n, n, key, rk, offs, dx2, nullptr, id2, nullptr, c->st));
   CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, c->st));
   CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3));
   PushArgs P = push_args(c, p, 0, 0);
-  CU(launch_interp_push(p.grid3, dx2, nullptr, n, id2, E, S, p.g, p.hc, P, c->st));
+  CU(launch_interp_push(p.grid3, D.x2, nullptr, n, D.id2, E, D.S, p.g, p.hc, P, c->st));
   CU(cudaMemcpyAsync(out, E, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  CU(cudaStreamSynchronize(c->st));
-  cudaFree(dx); cudaFree(dx2); cudaFree(E); cudaFree(id); cudaFree(counts); cudaFree(dc);
+  TRY(sync_stream(c, c->st));
   return PIF_OK;
 }
 
@@ -1304,8 +1410,10 @@ pif_status pif_debug_push(pif_ctx c, int which, double* x, double* v, const doub
   if (!c || !x || !v || !E || n < 1) return fail(PIF_ERR_ARG, "null argument");
   if (which < 0 || which > 1 || !c->plan[which].valid) return fail(PIF_ERR_ARG, "no such propagator");
   if (kicks < 0 || kicks > 2) return fail(PIF_ERR_ARG, "kicks must be 0, 1 or 2");
-  double* d;
-  CU(cudaMalloc(&d, 9 * n * sizeof(double)));
+  DeviceGuard dg(c->device);
+  DevBufs B(c->st);
+  double* d = nullptr;
+  CU(B.alloc(&d, 9 * n * sizeof(double)));
   CU(cudaMemcpyAsync(d, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
   CU(cudaMemcpyAsync(d + 3 * n, v, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
   CU(cudaMemcpyAsync(d + 6 * n, E, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
@@ -1313,8 +1421,7 @@ pif_status pif_debug_push(pif_ctx c, int which, double* x, double* v, const doub
   CU(launch_push_only(d, d + 3 * n, d + 6 * n, n, n, P, c->st));
   CU(cudaMemcpyAsync(x, d, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CU(cudaMemcpyAsync(v, d + 3 * n, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  CU(cudaStreamSynchronize(c->st));
-  cudaFree(d);
+  TRY(sync_stream(c, c->st));
   return PIF_OK;
 }
 

@@ -179,13 +179,12 @@ cudaError_t launch_schedule(const int* counts, const Sched& S, const Brick& g, i
                             cudaStream_t st);
 // keys per spreading brick
 inline int keys_per_brick(const Brick& g) { return g.m[0] * g.m[1] * g.m[2] * g.C; }
-cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,
-                                  int64_t stride, int64_t n, const int* key, const int* rank,
-                                  const int* offsets, double* x2, double* v2, int* id2, double* s2,
-                                  cudaStream_t st);
-cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id, int64_t stride,
-                                 int64_t n, const int* key, const int* rank, const int* offsets,
-                                 int* perm, double* x2, double* v2, int* id2, cudaStream_t st);
+// Physical counting sort (perm[offsets[key] + rank] = j, then gathers of x, v,
+// id and the optional strengths s; v / s may be null).
+cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id, const double* s,
+                                 int64_t stride, int64_t n, const int* key, const int* rank,
+                                 const int* offsets, int* perm, double* x2, double* v2, int* id2,
+                                 double* s2, cudaStream_t st);
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
                           const Sched& S, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st);
@@ -222,7 +221,8 @@ cudaError_t launch_correct_norms(const double* F, const double* Gn, const double
                                  int64_t n, double L, double* partials, double* out4,
                                  cudaStream_t st);
 cudaError_t launch_convert(double* d, float* f, int64_t count, bool to_float, cudaStream_t st);
-cudaError_t launch_check_finite(const double* a, int64_t count, int* flag, cudaStream_t st);
+// flag <- 1 on any non-finite a[i]; wrap_L > 0 also wraps a[i] into [0, wrap_L).
+cudaError_t launch_check_finite(double* a, int64_t count, double wrap_L, int* flag, cudaStream_t st);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 

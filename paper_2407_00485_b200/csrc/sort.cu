@@ -228,26 +228,8 @@ __global__ void k_schedule_fill(Sched S, Brick g, int M, int C) {
   }
 }
 
-__global__ void k_scatter_sorted(const double* __restrict__ x, const double* __restrict__ v,
-                                 const int* __restrict__ id, const double* __restrict__ s,
-                                 int64_t stride, int64_t n, const int* __restrict__ key,
-                                 const int* __restrict__ rank, const int* __restrict__ offsets,
-                                 double* __restrict__ x2, double* __restrict__ v2,
-                                 int* __restrict__ id2, double* __restrict__ s2) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  int64_t dst = offsets[key[j]] + rank[j];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    x2[d * stride + dst] = x[d * stride + j];
-    if (v) v2[d * stride + dst] = v[d * stride + j];
-  }
-  id2[dst] = id[j];
-  if (s) s2[dst] = s[j];
-}
-
-// Gather variant of the physical sort: perm[dst] = src (a 4-byte scatter),
-// then every array is gathered in destination order -- coalesced writes, and the
+// Physical sort by gather: perm[dst] = src (a 4-byte scatter), then every
+// array is gathered in destination order -- coalesced writes, and the
 // reads stay near-sequential because particles move less than a cell per step
 // (the partial-sector writes of a 52-byte-per-particle scatter are avoided).
 __global__ void k_scatter_index(int64_t n, const int* __restrict__ key,
@@ -258,19 +240,22 @@ __global__ void k_scatter_index(int64_t n, const int* __restrict__ key,
   perm[offsets[key[j]] + rank[j]] = (int)j;
 }
 
+// v / s (per-particle strengths of the debug type-1 export) may be null.
 __global__ void k_gather_sorted(const double* __restrict__ x, const double* __restrict__ v,
-                                const int* __restrict__ id, int64_t stride, int64_t n,
-                                const int* __restrict__ perm, double* __restrict__ x2,
-                                double* __restrict__ v2, int* __restrict__ id2) {
+                                const int* __restrict__ id, const double* __restrict__ s,
+                                int64_t stride, int64_t n, const int* __restrict__ perm,
+                                double* __restrict__ x2, double* __restrict__ v2,
+                                int* __restrict__ id2, double* __restrict__ s2) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t j = perm[i];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     x2[d * stride + i] = x[d * stride + j];
-    v2[d * stride + i] = v[d * stride + j];
+    if (v) v2[d * stride + i] = v[d * stride + j];
   }
   id2[i] = id[j];
+  if (s) s2[i] = s[j];
 }
 
 __global__ void k_iota(int* id, int64_t n) {
@@ -308,21 +293,13 @@ cudaError_t launch_schedule(const int* counts, const Sched& S, const Brick& g, i
   k_schedule_fill<<<nblk(S.nkeys, 256), 256, 0, st>>>(S, g, M, C);
   return cudaGetLastError();
 }
-cudaError_t launch_scatter_sorted(const double* x, const double* v, const int* id, const double* s,
-                                  int64_t stride, int64_t n, const int* key, const int* rank,
-                                  const int* offsets, double* x2, double* v2, int* id2, double* s2,
-                                  cudaStream_t st) {
-  if (n > 0)
-    k_scatter_sorted<<<nblk(n, 256), 256, 0, st>>>(x, v, id, s, stride, n, key, rank, offsets, x2,
-                                                   v2, id2, s2);
-  return cudaGetLastError();
-}
-cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id, int64_t stride,
-                                 int64_t n, const int* key, const int* rank, const int* offsets,
-                                 int* perm, double* x2, double* v2, int* id2, cudaStream_t st) {
+cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id, const double* s,
+                                 int64_t stride, int64_t n, const int* key, const int* rank,
+                                 const int* offsets, int* perm, double* x2, double* v2, int* id2,
+                                 double* s2, cudaStream_t st) {
   if (n > 0) {
     k_scatter_index<<<nblk(n, 256), 256, 0, st>>>(n, key, rank, offsets, perm);
-    k_gather_sorted<<<nblk(n, 256), 256, 0, st>>>(x, v, id, stride, n, perm, x2, v2, id2);
+    k_gather_sorted<<<nblk(n, 256), 256, 0, st>>>(x, v, id, s, stride, n, perm, x2, v2, id2, s2);
   }
   return cudaGetLastError();
 }

@@ -25,9 +25,36 @@
 //
 // Fragment layouts of m8n8k4.f64 (lane l, g = l >> 2, t = l & 3):
 //   A (8x4, row): A[g][t];  B (4x8, col): B[t][g];  C (8x8): C[g][2t], C[g][2t+1].
+#include <mutex>
+
 #include "pif_internal.cuh"
 
 namespace pif {
+
+// Per-device one-time launch setup: cudaFuncSetAttribute applies to the current
+// device only and the persistent grids are sized from its SM count, so the
+// result is cached per device (thread-safe).
+struct DevCache {
+  std::mutex mu;
+  int val[64] = {};
+};
+template <typename F>
+static cudaError_t dev_cached(DevCache& dc, int& out, F&& init) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(dc.mu);
+  if (!dc.val[dev]) {
+    int v = 0;
+    e = init(dev, v);
+    if (e != cudaSuccess) return e;
+    if (v < 1) return cudaErrorInvalidConfiguration;
+    dc.val[dev] = v;
+  }
+  out = dc.val[dev];
+  return cudaSuccess;
+}
 
 #ifndef PIF_SPREAD_MINB
 #define PIF_SPREAD_MINB 3  // 3 CTAs/SM (shared memory allows 3 for the 16^3 tile)
@@ -489,9 +516,6 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
         gx = gx < 0 ? gx + n : (gx >= n ? gx - n : gx);
         gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
         const double* src = grid3 + ((int64_t)gx * n + gy) * n;
-#ifdef PIF_EXP_NOLOAD  // timing experiment only: stale tiles after the first NBUF items
-        if (it.k < C::NBUF)
-#endif
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
@@ -585,9 +609,6 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
     prefetch(buf ^ 1, q + C::NW);  // xv[buf ^ 1] was released by the previous m-tile
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
-#ifdef PIF_EXP_NOSTAGE  // timing experiment only: stale psi rows after the first m-tile
-    if (q == wid)
-#endif
     stage(buf, cnt);
     const int tb = c.k % C::NBUF;
     mbar_wait(&S.full[tb], (c.k / C::NBUF) & 1);  // g tile of this item landed
@@ -630,11 +651,7 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
       e1 += __shfl_xor_sync(0xffffffffu, e1, o);
       e2 += __shfl_xor_sync(0xffffffffu, e2, o);
     }
-#ifdef PIF_EXP_NOPUSH  // timing experiment only: no push / stores
-    if (tq == 0 && gr < cnt && e0 == 1.2345e300) {
-#else
     if (tq == 0 && gr < cnt) {
-#endif
       const int64_t j = b + gr;
       if (Eout) {
         const int64_t k = id[j];
@@ -687,10 +704,10 @@ struct SlabCfg {
   static constexpr int KS = I::KS, NT = I::NT;
   static constexpr int SX = I::SX, SY = I::SY, SZ = I::SZ, OY = I::OY, OZ = I::OZ, WP = I::WP;
   static constexpr int CS = CSX;                    // columns per brick row (>= BX)
-  // doubles per slab: BY + 1 rows (the last one zero); one-row slabs (SBZ = 1)
-  // are padded to 4 (mod 16) so that the 4 slabs of a half-warp's fragment rows
-  // fall in different banks (conflict pattern checked exhaustively)
-  static constexpr int ZROW = ZR;                   // + a zero row per slab
+  // doubles per slab: BY (+ ZR padding) rows; one-row slabs (SBZ = 1) are padded
+  // to 4 (mod 16) so that the 4 slabs of a half-warp's fragment rows fall in
+  // different banks (conflict pattern checked exhaustively)
+  static constexpr int ZROW = ZR;                   // + a padding row per slab (bank spread)
   static constexpr int SLAB0 = (BY + ZROW) * CS * 3 * SBZ;
   static constexpr int SLAB = SBZ == 1 ? SLAB0 + ((20 - SLAB0 % 16) % 16) : SLAB0;
   static constexpr int NSZ = RZ / SBZ;              // slabs per tile
@@ -804,20 +821,6 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
       mbar_init(&S.full[b], 32);
       mbar_init(&S.done[b], C::NW);
     }
-  }
-  // The padded columns of an m-tile window's last k step (A = 0 there) read row
-  // BY of their slab: a zero row (ZROW), or else the next slab / the psi rows,
-  // which hold finite values once the whole buffer is zeroed here (a read racing
-  // a cp.async still combines finite halves: the high word carries the exponent)
-  if (C::ZROW) {
-    for (int i = threadIdx.x; i < C::NS * C::CS * 3 * SBZ; i += blockDim.x) {
-      const int sl = i / (C::CS * 3 * SBZ), e = i - sl * (C::CS * 3 * SBZ);
-      S.slab[sl][BY * C::CS * 3 * SBZ + e] = 0.0;
-    }
-  } else {
-    double2* z = reinterpret_cast<double2*>(&S.slab[0][0]);
-    const int n2 = (int)((sizeof(S.slab) + sizeof(S.psi)) / sizeof(double2));
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) z[i] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   const int lo = S.range[0], nitems = S.range[1] - S.range[0];
@@ -988,14 +991,25 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
     const double* pyr = wpsi + C::OY + gr * C::SY;
     int cx = tq, cy = 0;  // column 4 ks + tq of the window (RXm >= 4)
 #pragma unroll 2
-    for (int ks = 0; ks < KSm; ++ks) {
-      const double a = pxr[cx] * pyr[cy];  // cy == RYm (last step padding): py = 0
+    for (int ks = 0; ks < KSm - 1; ++ks) {
+      const double a = pxr[cx] * pyr[cy];
       const int off = (cy * C::CS + cx) * 3 * SBZ;
       cx += 4;
       if (cx >= RXm) {
         cx -= RXm;
         cy += 1;
       }
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, Pb[nt][off + d * SBZ]);
+    }
+    {
+      // last k step: columns past the window (cy == RYm) have A = 0 (py rows are
+      // zero-filled past the window) and read B from the window's last row, so
+      // every B operand is landed data of this item's slabs (no read outside them)
+      const double a = pxr[cx] * pyr[cy];
+      const int off = ((cy < RYm ? cy : RYm - 1) * C::CS + cx) * 3 * SBZ;
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
@@ -1047,16 +1061,18 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
                                  const Horner& hc, double* grid, cudaStream_t st) {
   const int T = 32 * SpreadCfg<A, B, Cz>::NW;
   const size_t smem = sizeof(Psi<A, B, Cz, kChunk>);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_spread<A, B, Cz, true, SUB>,
+  static DevCache cache;
+  int ok = 0;
+  cudaError_t e = dev_cached(cache, ok, [&](int, int& v) {
+    cudaError_t r = cudaFuncSetAttribute(k_spread<A, B, Cz, true, SUB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_spread<A, B, Cz, false, SUB>,
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(k_spread<A, B, Cz, false, SUB>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+    v = 1;
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   if (s)
     k_spread<A, B, Cz, true, SUB><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
   else
@@ -1067,13 +1083,6 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
                           const Sched& offsets, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st) {
-#ifdef PIF_SPREAD_SUB
-  // sub-brick spreading on the interpolation items (w = 13 tile, cell keys)
-  if (g.RI[0] == 14 && g.RI[1] == 14 && g.RI[2] == 16 && g.C > 1)
-    return spread_launch<14, 14, 16, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
-                                           g, hc, grid, st);
-#endif
-#ifndef PIF_NO_SPREAD_SUB_DENSE
   // dense w = 8 / w = 5 plans (>= 12 / 8 particles per cell, cell keys): spread
   // over the interpolation sub-bricks with the interpolation tile (10x10x8 /
   // 6x6x8 instead of 16x16x8 / 8^3: 2.6x / 1.8x fewer padded FMAs), the extra
@@ -1084,7 +1093,6 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
   if (g.C > 1 && g.RI[0] == 6 && g.RI[1] == 6 && g.RI[2] == 8)
     return spread_launch<6, 6, 8, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
                                         g, hc, grid, st);
-#endif
   const unsigned nbr = (unsigned)offsets.max_s;  // upper bound on spread items
 #define PIF_SPREAD(A, B, Cz)                                        \
   if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz)                \
@@ -1104,19 +1112,19 @@ static cudaError_t interp_launch(unsigned nsub, const double* grid3, double* x, 
                                  cudaStream_t st) {
   const int T = 32 * (InterpCfg<A, B, Cz>::NW + InterpCfg<A, B, Cz>::NP);
   const size_t smem = sizeof(InterpSmem<A, B, Cz>);
-  static int ctas = 0;  // persistent grid: SMs x resident CTAs per SM
-  if (!ctas) {
-    cudaError_t e = cudaFuncSetAttribute(k_interp_push<A, B, Cz>,
+  static DevCache cache;
+  int ctas = 0;  // persistent grid: SMs x resident CTAs per SM
+  cudaError_t e = dev_cached(cache, ctas, [&](int dev, int& v) {
+    int sms = 0, per = 0;
+    cudaError_t r = cudaFuncSetAttribute(k_interp_push<A, B, Cz>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 0, per = 0;
-    if (e == cudaSuccess) e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push<A, B, Cz>, T, smem);
-    if (e != cudaSuccess) return e;
-    if (per < 1) return cudaErrorInvalidConfiguration;
-    ctas = sms * per;
-  }
+    if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (r == cudaSuccess)
+      r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push<A, B, Cz>, T, smem);
+    v = sms * per;
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   const unsigned grid = nsub < (unsigned)ctas ? nsub : (unsigned)ctas;
   if (grid == 0) return cudaSuccess;
   k_interp_push<A, B, Cz><<<grid, T, smem, st>>>(grid3, x, v, stride, id, Eout, offsets, g, hc, P);
@@ -1131,19 +1139,20 @@ static cudaError_t interp_slab_launch(unsigned nsub, const double* grid3, double
   using C = SlabCfg<A, B, Cz, BX, BY, SBZ, CSX, ZR>;
   const int T = 32 * (C::NW + 1);
   const size_t smem = sizeof(SlabSmem<A, B, Cz, BX, BY, SBZ, CSX, ZR>);
-  static int sms = 0;
-  if (!sms) {
-    cudaError_t e = cudaFuncSetAttribute(k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX, ZR>,
+  static DevCache cache;
+  int sms = 0;
+  cudaError_t e = dev_cached(cache, sms, [&](int dev, int& v) {
+    int n_sm = 0, per = 0;
+    cudaError_t r = cudaFuncSetAttribute(k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX, ZR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, per = 0;
-    if (e == cudaSuccess) e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX, ZR>,
+    if (r == cudaSuccess) r = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (r == cudaSuccess)
+      r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_push_slab<A, B, Cz, BX, BY, SBZ, CSX, ZR>,
                                                         T, smem);
-    if (e != cudaSuccess) return e;
-    if (per < 1) return cudaErrorInvalidConfiguration;
-  }
+    v = per >= 1 ? n_sm : 0;
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   // persistent: one CTA per SM, each with a contiguous run of items
   const unsigned grid = nsub < (unsigned)sms ? nsub : (unsigned)sms;
   if (grid == 0) return cudaSuccess;
