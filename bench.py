@@ -9,10 +9,14 @@ ES interpolation fused with the KDK push.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1 (torchrun): weak scaling, 2^21 particles per GPU, one particle-
-decomposed problem (rho_hat allreduce over NCCL every step).  Timing: CUDA
-events on the library's stream around each step, L2 flushed (256 MB write)
-between steps outside the events, max over ranks.
+N > 1: one process per GPU (launched by torchrun, or -- without torchrun --
+bench.py re-executes itself under torch.distributed.run with N processes);
+weak scaling, 2^21 particles per GPU, one particle-decomposed problem
+(rho_hat allreduce over NCCL every step).  The line also carries "c3_strong":
+BASELINE configs[2] (TSI, 32^3 modes, 2^23 particles in total) split over the
+N GPUs (strong scaling of the particle decomposition).
+Timing: CUDA events on the library's stream around each step, L2 flushed
+(256 MB write) between steps outside the events, max over ranks.
 """
 from __future__ import annotations
 
@@ -20,6 +24,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -55,6 +60,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3-strong", action="store_true")
     ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS),
                     help="BASELINE.json configs index (default 1 = the headline workload)")
     args = ap.parse_args()
@@ -174,6 +180,63 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ ours --
+def timed_steps(P, sim, stream, steps, flush, world, dist):
+    """K steps bracketed by barrier + synchronize, CUDA events on the library's
+    stream per step, L2 flushed outside the events; returns (max-over-ranks
+    total ms, phases, launches)."""
+    import torch
+
+    P.pif_profile(sim.ctx, True)
+    P.pif_profile_read(sim.ctx, reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record(stream)
+        sim.step(1)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    phases, launches = P.pif_profile_read(sim.ctx, reset=True)
+    P.pif_profile(sim.ctx, False)
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=flush.device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), phases, launches
+
+
+def c3_strong(args, P, rank, world, local, nccl_id, flush, dist):
+    """BASELINE configs[2]: TSI, 32^3 modes, 2^23 particles in total split over
+    the world (particle decomposition, rho_hat allreduce), tol 1e-12, dt 0.05."""
+    import torch
+    from pif_inputs import make_case
+
+    case, N, n_global, tol, dt = CONFIGS[2]
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    p, x0, v0 = make_case(case, n_global, 2)  # the same global problem on every N
+    sim = P.Simulation(P.physics(p.L, p.q_over_m, p.total_charge, p.B, p.A, p.c),
+                       P.propagator("pif", N, dt, tol=tol), None, n_particles=n_global,
+                       device=local, rank=rank, world=world, space_size=world, nccl_id=nccl_id,
+                       stream=stream)
+    a, c = sim.first, sim.n_local
+    sim.set_state(torch.from_numpy(x0[:, a:a + c].copy()).to(dev), torch.from_numpy(v0[:, a:a + c].copy()).to(dev))
+    sim.step(args.warmup)
+    total_ms, phases, launches = timed_steps(P, sim, stream, args.steps, flush, world, dist)
+    sim.close()
+    return {"workload": f"{case}_3d3v_{N}^3modes_{n_global}particles_total_tol{tol:g}_dt{dt}",
+            "metric": "particles pushed/s (PIF step)", "unit": "particles/s", "scaling": "strong",
+            "n_particles_global": n_global, "n_gpus": world,
+            "value": n_global * args.steps / (total_ms / 1000.0),
+            "ms_per_step": total_ms / args.steps,
+            "phase_ms_per_step_rank0": {k: v / args.steps for k, v in phases.items() if v > 0}}
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
@@ -199,39 +262,18 @@ def run_ours(args, rank, world, local):
                        device=local, rank=rank, world=world, space_size=world, nccl_id=nccl_id,
                        stream=stream)
     w, beta, n_up = sim.plan_info(0)
+    comm = sim.comm_info()
     xd = torch.from_numpy(x0).to(dev)
     vd = torch.from_numpy(v0).to(dev)
     sim.set_state(xd, vd)
     sim.step(args.warmup)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     torch.cuda.synchronize()
-    P.pif_profile(sim.ctx, True)
-    P.pif_profile_read(sim.ctx, reset=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    for e0, e1 in evs:
-        flush.zero_()
-        e0.record(stream)
-        sim.step(1)
-        e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    total_ms, phases, launches = timed_steps(P, sim, stream, args.steps, flush, world, dist)
     clocks = clk.stop()
-    phases, launches = P.pif_profile_read(sim.ctx, reset=True)
-    P.pif_profile(sim.ctx, False)
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
     value = n_global * args.steps / (total_ms / 1000.0)
 
     # roofline of the dominant kernel (per launch; one launch per step)
@@ -278,6 +320,13 @@ def run_ours(args, rank, world, local):
         nb = 2 * 3 * sim.n_local * 8
         e2e = {"value": n_global * ksteps / float(el.item()), "unit": "particles/s",
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "steps": ksteps}
+    n_local = sim.n_local
+    sim.close()
+    del xd, vd
+
+    strong = None
+    if CFG == 1 and not args.no_c3_strong:
+        strong = c3_strong(args, P, rank, world, local, nccl_id, flush, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -286,7 +335,6 @@ def run_ours(args, rank, world, local):
         cpu = {"value": rate, "unit": "particles/s", "cores": threads, "kind": "oracle",
                "sample": f"{n_sample} of the {N_PER_GPU} configs[{CFG}] {CASE} particles, one KDK "
                          f"step of the exact O(N_p N^3) NUDFT PIF at N={N_MODES} ({secs:.1f} s)"}
-    sim.close()
     if rank == 0:
         line = {
             "metric": "particles pushed/s (PIF step)", "value": value, "unit": "particles/s",
@@ -294,16 +342,31 @@ def run_ours(args, rank, world, local):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(), "n_particles_global": n_global,
+                       "n_particles_per_gpu": n_local,
                        "modes": N_MODES, "nufft_tol": TOL, "es_width": w, "es_beta": beta,
                        "upsampled_grid": n_up, "dt": DT, "l2": "flushed (256 MB write) between steps",
                        "parallelism": f"particle-decomposition x{world} (rho_hat allreduce)"},
-            "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "nccl": comm, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "phase_ms_per_step": {k: v / args.steps for k, v in phases.items() if v > 0},
+            "c3_strong": strong,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 without torchrun: re-execute this script under
+    torch.distributed.run with N processes (one per GPU) on 127.0.0.1; rank 0
+    prints the JSON line."""
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -312,8 +375,13 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if args.gpus != world and world == 1 and args.gpus > 1:
-        sys.exit("--gpus N > 1 must be launched with torchrun --nproc-per-node N")
+    if args.gpus > 1 and world == 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if world > 1:
+        # NCCL INIT logging (to stderr) shows every communicator's nranks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     run_ours(args, rank, world, local)
 
 

@@ -208,6 +208,12 @@ pif_status pif_nccl_unique_id(void* out128);
    beta, upsampled grid n). */
 pif_status pif_plan_info(pif_ctx ctx, int which, int32_t* w, double* beta, int32_t* n_up);
 
+/* Communicator sizes as NCCL reports them (ncclCommCount): world, space group
+   (rho_hat all-reduce) and time group (parareal hand-off); 1, 1, 1 when
+   world == 1.  Host-only query. */
+pif_status pif_comm_info(pif_ctx ctx, int32_t* world_nranks, int32_t* space_nranks,
+                         int32_t* time_nranks);
+
 /* Phase profiling (tracing).  While enabled, every phase of a step is bracketed
    by CUDA events on the stream (no synchronisation).  pif_profile_read
    synchronises, returns the summed device time in ms per phase since the last

@@ -95,19 +95,25 @@ def nudft_type1(x: np.ndarray, s: np.ndarray, N: int, L: float) -> np.ndarray:
 
 
 def nudft_type2_complex(c: np.ndarray, x: np.ndarray, N: int, L: float) -> np.ndarray:
-    """out_j = sum_{k in K_N} c_k exp(+i k . x_j)   (eq. gather_pif)."""
+    """out_j = sum_{k in K_N} c_k exp(+i k . x_j)   (eq. gather_pif).
+
+    c: (N,N,N) -> out (N_p,); or a stack (D,N,N,N) of D coefficient arrays
+    evaluated at the same positions (the three field components) -> (D, N_p)."""
     k = wavenumbers(N, L)
-    out = np.empty(x.shape[1], dtype=np.complex128)
+    cs = c.reshape(-1, N, N, N)
+    D = cs.shape[0]
+    out = np.empty((D, x.shape[1]), dtype=np.complex128)
     for a in range(0, x.shape[1], _chunk(N)):
         sl = slice(a, a + _chunk(N))
         ex = np.exp(1j * np.outer(x[0, sl], k))
         ey = np.exp(1j * np.outer(x[1, sl], k))
         ez = np.exp(1j * np.outer(x[2, sl], k))
-        # y[j,(a,b)] = sum_c c[a,b,c] ez[j,c]  (a contraction over c), then
-        # out_j = sum_{a,b} y[j,a,b] ex[j,a] ey[j,b]
-        y = (ez @ c.reshape(N * N, N).T).reshape(-1, N, N)
-        out[sl] = np.sum(y * ex[:, :, None] * ey[:, None, :], axis=(1, 2))
-    return out
+        # y[j,d,(a,b)] = sum_c c_d[a,b,c] ez[j,c]  (a contraction over c), then
+        # out_dj = sum_{a,b} y[j,d,a,b] ex[j,a] ey[j,b]
+        y = (ez @ cs.reshape(D * N * N, N).T).reshape(-1, D, N, N)
+        exy = ex[:, :, None] * ey[:, None, :]
+        out[:, sl] = np.sum(y * exy[:, None], axis=(2, 3)).T
+    return out[0] if c.ndim == 3 else out
 
 
 def nudft_type2(c: np.ndarray, x: np.ndarray, N: int, L: float) -> np.ndarray:
@@ -147,7 +153,7 @@ def field_from_rho_tilde(rho_tilde: np.ndarray, x: np.ndarray, N: int, L: float,
     """E(x_j) = Re sum_k S_k E_k exp(i k x_j)  (eq. gather_pif) [R2]."""
     E_k = poisson_spectral(rho_tilde, N, L, order)
     S = shape_factor(N, L, order)
-    E = np.stack([nudft_type2(S * E_k[d], x, N, L) for d in range(3)])
+    E = nudft_type2(S[None] * E_k, x, N, L)  # the three components, shape (3, N_p)
     return E, E_k
 
 

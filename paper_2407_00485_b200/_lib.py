@@ -74,6 +74,7 @@ _sig = {
     "pif_debug_type2": [_ctx, C.c_int, _dp, _dp, _i64, _dp],
     "pif_debug_push": [_ctx, C.c_int, _dp, _dp, _dp, _i64, C.c_int, C.c_int],
     "pif_profile": [_ctx, C.c_int],
+    "pif_comm_info": [_ctx, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
     "pif_get_rho": [_ctx, _dp],
     "pif_debug_parareal_protocol": [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p,
                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32),
@@ -266,6 +267,13 @@ def pif_debug_push(ctx, which, x, v, E, kicks, drift):
         assert a.dtype == np.float64 and a.flags.c_contiguous
     _check("pif_debug_push", lib.pif_debug_push(ctx, which, x.ctypes.data, v.ctypes.data,
                                                 E.ctypes.data, x.shape[1], kicks, drift))
+
+
+def pif_comm_info(ctx):
+    """-> {"world_nranks", "space_nranks", "time_nranks"} from ncclCommCount."""
+    a, b, d = C.c_int32(), C.c_int32(), C.c_int32()
+    _check("pif_comm_info", lib.pif_comm_info(ctx, C.byref(a), C.byref(b), C.byref(d)))
+    return {"world_nranks": a.value, "space_nranks": b.value, "time_nranks": d.value}
 
 
 PHASES = ("sort", "spread", "fft_fwd", "box", "allreduce", "poisson", "fft_inv", "interp_push",

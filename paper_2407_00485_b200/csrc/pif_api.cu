@@ -1259,6 +1259,22 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
   return PIF_OK;
 }
 
+pif_status pif_comm_info(pif_ctx c, int32_t* world_nranks, int32_t* space_nranks,
+                        int32_t* time_nranks) {
+  if (!c || !world_nranks || !space_nranks || !time_nranks) return fail(PIF_ERR_ARG, "null argument");
+  *world_nranks = *space_nranks = *time_nranks = 1;
+  if (c->world == 1) return PIF_OK;
+  if (c->nccl_broken) return fail(PIF_ERR_NCCL, "communicators were aborted by an earlier NCCL failure");
+  int a = 0, b = 0, d = 0;
+  NC(ncclCommCount(c->comm_world, &a));
+  NC(ncclCommCount(c->comm_space, &b));
+  NC(ncclCommCount(c->comm_time, &d));
+  *world_nranks = a;
+  *space_nranks = b;
+  *time_nranks = d;
+  return PIF_OK;
+}
+
 pif_status pif_profile(pif_ctx c, int enable) {
   if (!c) return fail(PIF_ERR_ARG, "null context");
   c->prof = enable != 0;

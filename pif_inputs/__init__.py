@@ -33,6 +33,8 @@ __all__ = [
     "landau_state",
     "tsi_state",
     "penning_state",
+    "landau_state_quiet",
+    "tsi_state_quiet",
     "make_case",
     "CONFIGS",
 ]
@@ -135,6 +137,48 @@ def penning_state(n_particles: int, seed: int, L: float = 25.0, sd=(2.0, 1.0, 3.
             bad = (xd < 0) | (xd >= L)
         x[d] = xd
     v = rng.standard_normal((3, n_particles))
+    return x, v
+
+
+def _halton(n: int, base: int) -> np.ndarray:
+    """Radical inverse of 1..n in `base` (one coordinate of a Halton sequence)."""
+    i = np.arange(1, n + 1)
+    f = np.ones(n)
+    r = np.zeros(n)
+    while np.any(i > 0):
+        f = f / base
+        r = r + f * (i % base)
+        i = i // base
+    return r
+
+
+def _ndtri(u: np.ndarray) -> np.ndarray:
+    from scipy.special import ndtri
+    return ndtri(u)
+
+
+def landau_state_quiet(n_particles: int, alpha: float = 0.05, kw: float = 0.5):
+    """Landau damping state with a low-discrepancy ("quiet") load: the recipe of
+    landau_state with the uniform draws u replaced by the 6-D Halton sequence
+    (bases 2, 3, 5 for x, y, z through the inverse CDF; 7, 11, 13 for v through
+    the inverse normal CDF).  Used by the statistical rate pins of the oracle
+    (R23): sampling noise in the resonant mode falls from ~1/sqrt(N_p)
+    to ~log(N_p)/N_p, so 2^16 particles resolve the damping rate."""
+    L = 2.0 * math.pi / kw
+    x = np.stack([_invert_cdf(_halton(n_particles, b), L, alpha, kw) for b in (2, 3, 5)])
+    v = np.stack([_ndtri(_halton(n_particles, b)) for b in (7, 11, 13)])
+    return x, v
+
+
+def tsi_state_quiet(n_particles: int, alpha: float = 0.01, kw: float = 0.5,
+                    sigma: float = 0.1, vb: float = math.pi / 2):
+    """Two-stream state with the Halton load (bases 2, 3 uniform x, y; 5 inverse
+    CDF z; 7, 11, 13 thermal v; 17 the beam sign, u < 1/2 -> -vb)."""
+    L = 2.0 * math.pi / kw
+    x = np.stack([_halton(n_particles, 2) * L, _halton(n_particles, 3) * L,
+                  _invert_cdf(_halton(n_particles, 5), L, alpha, kw)])
+    v = sigma * np.stack([_ndtri(_halton(n_particles, b)) for b in (7, 11, 13)])
+    v[2] += np.where(_halton(n_particles, 17) < 0.5, -1.0, 1.0) * vb
     return x, v
 
 

@@ -1,6 +1,7 @@
 """Multi-GPU worker (one process per GPU, launched by torchrun) for
 tests/test_gpu_multi.py.  Every rank runs the distributed path through the C
-ABI; rank 0 also runs the single-GPU reference and checks the results.
+ABI; rank 0 compares the gathered result with the CPU oracle (exact NUDFT PIF /
+oracle parareal) and with the single-GPU run of the same problem.
 
   torchrun --nproc-per-node N tests/mp_worker.py {space|parareal|spacetime}
 """
@@ -15,6 +16,7 @@ import torch.distributed as dist
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import oracle as O  # noqa: E402
 import paper_2407_00485_b200 as P  # noqa: E402
 from pif_inputs import landau_physics, landau_state  # noqa: E402
 
@@ -80,6 +82,15 @@ def run_space(rank, world, local, nid, fp32=False):
                    dW=float(np.abs(W - Wr).max() / Wr.sum()), dke=abs(ke - ker) / ker,
                    dmom=float(np.abs(mom - momr).max() / (abs(ker) ** 0.5)))
         ref.close()
+        # the oracle: exact NUDFT PIF over all particles
+        ph = O.PhysicsParams.from_inputs(landau_physics())
+        prop = O.Propagator("pif", 8, 0.05)
+        xo, vo = O.run(x0, v0, steps, prop, ph)
+        Wo, keo, momo, ceo = O.diagnostics(xo, vo, prop, ph)
+        res.update(dx_oracle=float(np.abs(O.min_image(xs.cpu().numpy() - xo, L)).max() / L),
+                   dv_oracle=float(np.abs(vs.cpu().numpy() - vo).max() / np.abs(vo).max()),
+                   dW_oracle=float(np.abs(W - Wo).max() / Wo.sum()),
+                   dke_oracle=abs(ke - keo) / keo)
     return res
 
 
@@ -124,6 +135,16 @@ def run_parareal(rank, world, local, nid, space_size, blocks=1):
                    dv=float((vl - vr).abs().max().item() / vr.abs().max().item()),
                    t_total=rep["t_total"], t_comm=rep["t_comm"])
         ref.close()
+        # the oracle's parareal (eq. parareal_correction) with the
+        # exact NUDFT PIF fine and CIC-PIC coarse propagators
+        ph = O.PhysicsParams.from_inputs(landau_physics())
+        F = O.make_propagator_fn(O.Propagator("pif", 8, dtf), ph, nf)
+        G = O.make_propagator_fn(O.Propagator("pic", 8, dtg), ph, int(round(nf * dtf / dtg)))
+        ores = O.parareal_blocks((x0, v0), lambda b: F, lambda b: G, T, blocks, T, 1e-6, L=L)
+        xo, vo = ores[-1].U[T]
+        res.update(retired_oracle=ores[-1].retired_at, iters_oracle=sum(r.iterations for r in ores),
+                   dx_oracle=float(np.abs(O.min_image(xl.cpu().numpy() - xo, L)).max() / L),
+                   dv_oracle=float(np.abs(vl.cpu().numpy() - vo).max() / np.abs(vo).max()))
     return res
 
 

@@ -1,6 +1,7 @@
 """Multi-GPU paths on one box (skipped with fewer GPUs): particle decomposition
 (rho_hat allreduce over NCCL) and the pipelined parareal (NCCL send/recv of the
-particle state between time ranks), each against the single-GPU result."""
+particle state between time ranks), each against the CPU oracle (exact NUDFT
+PIF / oracle parareal) and the single-GPU result."""
 import json
 import os
 import subprocess
@@ -30,6 +31,8 @@ def launch(nproc, mode, port):
 @pytest.mark.skipif(ngpu() < 2, reason="needs 2 GPUs")
 def test_space_decomposition_2gpu():
     r = launch(2, "space", 29611)
+    assert r["dx_oracle"] <= 1e-10 and r["dv_oracle"] <= 1e-10, r
+    assert r["dW_oracle"] <= 1e-10 and r["dke_oracle"] <= 1e-10, r
     assert r["dx"] <= 1e-12 and r["dv"] <= 1e-12, r
     assert r["dW"] <= 1e-12 and r["dke"] <= 1e-12, r
 
@@ -37,6 +40,8 @@ def test_space_decomposition_2gpu():
 @pytest.mark.skipif(ngpu() < 2, reason="needs 2 GPUs")
 def test_pipelined_parareal_2gpu():
     r = launch(2, "parareal", 29612)
+    assert r["retired"] == r["retired_oracle"] and r["iters"] == r["iters_oracle"], r
+    assert r["dx_oracle"] <= 1e-9 and r["dv_oracle"] <= 1e-9, r
     assert r["retired"] == r["retired_ref"] and r["iters"] == r["iters_ref"], r
     assert r["dx"] <= 1e-9 and r["dv"] <= 1e-9, r
 
@@ -44,6 +49,8 @@ def test_pipelined_parareal_2gpu():
 @pytest.mark.skipif(ngpu() < 4, reason="needs 4 GPUs")
 def test_spacetime_parareal_4gpu():
     r = launch(4, "spacetime", 29613)
+    assert r["retired"] == r["retired_oracle"] and r["iters"] == r["iters_oracle"], r
+    assert r["dx_oracle"] <= 1e-9 and r["dv_oracle"] <= 1e-9, r
     assert r["retired"] == r["retired_ref"] and r["iters"] == r["iters_ref"], r
     assert r["dx"] <= 1e-9 and r["dv"] <= 1e-9, r
 
@@ -53,11 +60,14 @@ def test_space_decomposition_fp32_allreduce_2gpu():
     """f3: rho_hat all-reduced in fp32: same trajectories to single-precision level."""
     r = launch(2, "space32", 29614)
     assert 0 < r["dx"] <= 1e-6 and r["dv"] <= 1e-5, r
+    assert r["dx_oracle"] <= 1e-6 and r["dv_oracle"] <= 1e-5, r
 
 
 @pytest.mark.skipif(ngpu() < 2, reason="needs 2 GPUs")
 def test_multiblock_pipelined_parareal_2gpu():
     """f1: 3 windows of pipelined parareal on 2 time ranks == serial schedule."""
     r = launch(2, "blocks", 29615)
+    assert r["retired"] == r["retired_oracle"] and r["iters"] == r["iters_oracle"], r
+    assert r["dx_oracle"] <= 1e-9 and r["dv_oracle"] <= 1e-9, r
     assert r["retired"] == r["retired_ref"] and r["iters"] == r["iters_ref"], r
     assert r["dx"] <= 1e-9 and r["dv"] <= 1e-9, r

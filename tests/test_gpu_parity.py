@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from dispersion import dispersion_root
 from pif_inputs import landau_physics, landau_state, penning_physics, penning_state, tsi_physics, tsi_state
 
 pytestmark = pytest.mark.gpu
@@ -302,30 +303,6 @@ def test_multiblock_parareal_matches_oracle():
 
 
 # ------------------------------------------------------------------ physics --
-def _dispersion_root(N, L, kk, guess, sigma=1.0, vb=0.0):
-    """Shape-corrected kinetic dispersion 1 + (S^2/k^2) chi(omega) = 0 for Maxwellian
-    beams (two half-density beams at +-vb, thermal speed sigma); Z = i sqrt(pi) w."""
-    from scipy.special import wofz
-    h = L / N
-    S2 = (math.sin(kk * h / 2) / (kk * h / 2)) ** 4
-
-    def chi(w):
-        tot = 0.0
-        beams = [(0.5, vb), (0.5, -vb)] if vb else [(1.0, 0.0)]
-        for frac, u in beams:
-            z = (w - kk * u) / (math.sqrt(2) * kk * sigma)
-            tot += frac * (1 + z * 1j * math.sqrt(math.pi) * wofz(z)) / sigma ** 2
-        return tot
-
-    w = guess
-    for _ in range(80):
-        D = 1 + S2 / kk ** 2 * chi(w)
-        dw = 1e-7 * (1 + abs(w))
-        dD = (1 + S2 / kk ** 2 * chi(w + dw) - D) / dw
-        w = w - D / dD
-    return w
-
-
 def _resonant_energy(sim, N, L, q):
     rho = P.pif_get_rho(sim.ctx, N)
     k1 = 2 * math.pi / L
@@ -352,7 +329,7 @@ def test_landau_damping_rate_C2():
         ts.append(s * dt)
         ws.append(_resonant_energy(sim, N, phys.L, phys.total_charge / n))
     t, W = np.array(ts), np.array(ws)
-    root = _dispersion_root(N, phys.L, 0.5, 1.4 - 0.15j)
+    root = dispersion_root(N, phys.L, 0.5, 1.4 - 0.15j)
     assert abs(root.real - 1.41322) < 2e-4 and abs(root.imag + 0.15448) < 2e-4
     sel = t >= 1.0
 
@@ -384,7 +361,7 @@ def test_two_stream_growth_rate_C3():
             ts.append(s * dt)
             ws.append(_resonant_energy(sim, N, phys.L, phys.total_charge / n))
     slope = np.polyfit(np.array(ts), np.log(np.array(ws)), 1)[0] / 2
-    root = _dispersion_root(N, phys.L, 0.5, 0.3j, sigma=0.1, vb=math.pi / 2)
+    root = dispersion_root(N, phys.L, 0.5, 0.3j, sigma=0.1, vb=math.pi / 2)
     assert abs(root.imag - 0.31615) < 2e-3, root
     assert abs(slope - root.imag) < 0.10 * root.imag, (slope, root)
 
@@ -418,3 +395,111 @@ def test_error_paths():
     sim.step(2)
     x, v = sim.get_state()
     assert torch.isfinite(x).all() and torch.isfinite(v).all()
+
+
+# ------------------------------------------ round-2 parity gaps --
+def _cluster_state(n, L, center, sigma, frac, seed):
+    """Penning-like crowded cloud: a fraction `frac` of the particles in a tight
+    Gaussian (sigma in length units) around `center`, the rest uniform."""
+    rng = np.random.default_rng(seed)
+    m = int(frac * n)
+    x = np.empty((3, n))
+    x[:, :m] = np.mod(center + sigma * rng.standard_normal((3, m)), L)
+    x[:, m:] = rng.random((3, n - m)) * L
+    v = rng.standard_normal((3, n))
+    return x, v
+
+
+def test_crowded_bricks_item_splitting():
+    """Work-item splitting of crowded bricks (Sched: > kSpreadItem = 4096 particles
+    per spreading brick, > kInterpItem = 1024 per interpolation sub-brick, the C4
+    Penning-core regime): 2^17 particles, 85 % of them in a cloud of sigma = 0.4
+    (about half an upsampled cell, n = 32) -- type-1 / type-2 within 10 eps and 20
+    Boris steps within 1e-10 of the exact NUDFT oracle."""
+    phys = penning_physics()
+    n, N, tol = 1 << 17, 8, 1e-12
+    x, v = _cluster_state(n, phys.L, phys.L / 2, 0.4, 0.85, 21)
+    h = phys.L / 32  # upsampled cell (w = 13 -> n = 32)
+    cells = np.floor(x / h).astype(int)
+    sub = cells // np.array([2, 2, 4])[:, None]   # interpolation sub-bricks (2x2x4 cells)
+    brk = cells // 4                               # spreading bricks (4^3 cells)
+    assert np.unique(sub, axis=1, return_counts=True)[1].max() > 4 * 1024
+    assert np.unique(brk, axis=1, return_counts=True)[1].max() > 4 * 4096
+    sim = sim_for(phys, P.propagator("pif", N, 0.003125, tol=tol), n=n)
+    assert sim.plan_info(0)[2] == 32
+    s = np.random.default_rng(22).standard_normal(n)
+    assert rel_l2(P.pif_debug_type1(sim.ctx, 0, x, s, N), O.nudft_type1(x, s, N, phys.L)) <= 10 * tol
+    c = np.random.default_rng(23).standard_normal((N, N, N)) + 1j * np.random.default_rng(24).standard_normal((N, N, N))
+    assert rel_l2(P.pif_debug_type2(sim.ctx, 0, c, x), O.nudft_type2(c, x, N, phys.L)) <= 10 * tol
+    sim.close()
+    xg, vg, W, ke, mom, ce, _ = run_gpu(phys, P.propagator("pif", N, 0.003125, tol=tol), x, v, 20)
+    xr, vr = O.run(x, v, 20, O.Propagator("pif", N, 0.003125), O.PhysicsParams.from_inputs(phys))
+    assert np.abs(O.min_image(xg - xr, phys.L)).max() <= 1e-10 * phys.L
+    assert np.abs(vg - vr).max() <= 1e-10 * np.abs(vr).max()
+
+
+def test_C4_full_size_sampled_modes_and_particles():
+    """BASELINE configs[3] size (Penning, 64^3 modes, upsampled n = 128, 2^24
+    particles, tol 1e-12) in the bench's launch configuration (--config 3):
+    type-1 on 16 sampled modes against per-mode direct sums, type-2 on 512
+    sampled particles, both within 10 eps.  The C4 cloud core (~1300 particles
+    per upsampled cell) also exercises the crowded-brick item splitting."""
+    phys = penning_physics()
+    n, N, tol = 1 << 24, 64, 1e-12
+    x, _ = penning_state(n, 3)
+    sim = sim_for(phys, P.propagator("pif", N, 0.003125, tol=tol), n=n)
+    assert sim.plan_info(0)[2] == 128
+    s = np.random.default_rng(31).standard_normal(n)
+    got = P.pif_debug_type1(sim.ctx, 0, x, s, N)
+    rng = np.random.default_rng(32)
+    idx = rng.integers(0, N, size=(16, 3))
+    k = 2 * math.pi / phys.L * (idx - N // 2)
+    ref = np.array([np.sum(s * np.exp(-1j * (kk @ x))) for kk in k])
+    assert rel_l2(got[idx[:, 0], idx[:, 1], idx[:, 2]], ref) <= 10 * tol
+    del got
+    c = rng.standard_normal((N, N, N)) + 1j * rng.standard_normal((N, N, N))
+    sel = rng.choice(n, 512, replace=False)
+    out = P.pif_debug_type2(sim.ctx, 0, c, x)
+    assert rel_l2(out[sel], O.nudft_type2(c, x[:, sel], N, phys.L)) <= 10 * tol
+
+
+@pytest.mark.parametrize("tol,w", [(1e-7, 8), (1e-4, 5)])
+def test_dense_tiles_steps_vs_oracle(tol, w):
+    """The dense slab tiles (w = 8: 10x10x8, w = 5: 6x6x8; chosen at >= 12 / 8
+    particles per upsampled cell) through pif_step: 16 particles per cell on the
+    16^3 grid (N = 8), 5 Landau steps of dt = 0.05 against the exact oracle.
+    Tolerance from the NUFFT bound: each kick's field has relative L2 error
+    <= 10 eps (R20), so the velocity change Dv = sum_k dt E_k has relative error
+    <= 10 eps * sum_k |E_k| / |sum_k E_k| (~1: the field barely turns in 5 dt =
+    0.25 << the plasma period 4.4), and the field-driven displacement
+    x - (x0 + K dt v0) likewise; trajectory feedback is second order.  Written
+    bound: 2 x 10 eps on both."""
+    phys = landau_physics()
+    n, N, dt, K = 16 * 16 ** 3, 8, 0.05, 5
+    x0, v0 = landau_state(n, 41)
+    sim = sim_for(phys, P.propagator("pif", N, dt, tol=tol), n=n)
+    assert sim.plan_info(0)[0] == w and sim.plan_info(0)[2] == 16
+    sim.close()
+    x, v, *_ = run_gpu(phys, P.propagator("pif", N, dt, tol=tol), x0, v0, K)
+    xr, vr = O.run(x0, v0, K, O.Propagator("pif", N, dt), O.PhysicsParams.from_inputs(phys))
+    dv_ref = vr - v0
+    assert np.linalg.norm(v - vr) <= 2 * 10 * tol * np.linalg.norm(dv_ref)
+    disp_ref = O.min_image(xr - (x0 + K * dt * v0), phys.L)
+    assert np.linalg.norm(O.min_image(x - xr, phys.L)) <= 2 * 10 * tol * np.linalg.norm(disp_ref)
+
+
+def test_set_state_wraps_positions_outside_the_box():
+    """Positions given outside [0, L) (here x + 2L and x - 2L, i.e. 2.5 L and
+    -1.5 L for x = L/2) are wrapped periodically by pif_set_state: the state and
+    the next steps equal those of the wrapped input."""
+    phys = landau_physics()
+    x0, v0 = landau_state(4096, 42)
+    xs = x0.copy()
+    xs[0, ::3] += 2 * phys.L
+    xs[1, 1::3] -= 2 * phys.L
+    xs[2, 2::5] += 7 * phys.L
+    a = run_gpu(phys, P.propagator("pif", 8, 0.05, tol=1e-12), x0, v0, 3)
+    b = run_gpu(phys, P.propagator("pif", 8, 0.05, tol=1e-12), xs, v0, 3)
+    assert np.abs(O.min_image(a[0] - b[0], phys.L)).max() <= 1e-13 * phys.L
+    assert np.abs(a[1] - b[1]).max() <= 1e-13 * np.abs(a[1]).max()
+    assert np.all((b[0] >= 0) & (b[0] < phys.L))

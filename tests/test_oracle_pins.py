@@ -67,6 +67,23 @@ def test_type2_brute_force():
     assert np.allclose(O.nudft_type2(c, x, N, L), got.real, rtol=0, atol=0)
 
 
+def test_type2_stacked_coefficients_brute_force():
+    """A stack of D coefficient arrays (the field components) at the same
+    positions: row d is the brute-force sum for c_d."""
+    rng = np.random.default_rng(3)
+    N, L, n, D = 4, 7.0, 4, 3
+    x = rng.random((3, n)) * L
+    c = rng.standard_normal((D, N, N, N)) + 1j * rng.standard_normal((D, N, N, N))
+    got = O.nudft_type2_complex(c, x, N, L)
+    assert got.shape == (D, n)
+    m = list(range(-N // 2, N // 2))
+    for d in range(D):
+        for j in range(n):
+            ref = sum(c[d, ia, ib, ic] * cmath.exp(1j * (2 * math.pi / L) * (a * x[0, j] + b * x[1, j] + cc * x[2, j]))
+                      for ia, a in enumerate(m) for ib, b in enumerate(m) for ic, cc in enumerate(m))
+            assert abs(got[d, j] - ref) <= 1e-12 * abs(ref)
+
+
 def test_type1_single_particle_at_origin():
     """A point at x = 0: every exponential is 1."""
     out = O.nudft_type1(np.zeros((3, 1)), np.array([2.5]), 6, L4PI)
@@ -329,24 +346,6 @@ def test_parareal_exact_after_Ns_iterations_pic_coarse():
 
 
 # --------------------------------------------------------------- physics ---
-def _landau_root(N, L, kk=0.5):
-    """Shape-corrected kinetic dispersion 1 + (S^2/k^2)(1 + zeta Z(zeta)) = 0,
-    zeta = omega / (sqrt 2 k), Z = i sqrt(pi) w(zeta) (textbook Landau relation)."""
-    from scipy.special import wofz
-    h = L / N
-    S2 = (math.sin(kk * h / 2) / (kk * h / 2)) ** 4
-
-    def D(w):
-        z = w / (math.sqrt(2) * kk)
-        return 1 + (S2 / kk ** 2) * (1 + z * 1j * math.sqrt(math.pi) * wofz(z))
-
-    w = 1.4 - 0.15j
-    for _ in range(60):
-        dw = 1e-7
-        w = w - D(w) / ((D(w + dw) - D(w)) / dw)
-    return w
-
-
 def test_cold_plasma_oscillation_closed_form():
     """Whole-step pin, deterministic: a cold (v = 0) lattice plasma with a small
     sinusoidal displacement z_j = z0_j + delta sin(k z0_j) oscillates at the
