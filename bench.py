@@ -45,7 +45,10 @@ CONFIGS = {1: ("landau", 32, 1 << 21, 1e-12, 0.05),     # C2
            4: ("landau", 64, 1 << 26, 1e-7, 0.003125),    # C5 fine propagator (1 GPU)
            5: ("landau", 64, 1 << 22, 1e-7, 0.003125),    # C5-reduced parareal fine propagator
            6: ("landau", 64, 1 << 22, 1e-4, 0.05),        # C5-reduced parareal coarse (PIF) propagator
-           7: ("landau", 64, 1 << 26, 1e-4, 0.05)}        # C5 coarse (PIF, eps 1e-4) propagator (1 GPU)
+           7: ("landau", 64, 1 << 26, 1e-4, 0.05),        # C5 coarse (PIF, eps 1e-4) propagator (1 GPU)
+           8: ("landau", 64, 1 << 26, 1e-4, 0.05),        # C5 coarse propagator in fp32 (PIF_FLAG_FP32)
+           9: ("landau", 64, 1 << 22, 1e-4, 0.05)}        # C5-reduced coarse propagator in fp32
+FP32_CONFIGS = (8, 9)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 SM_COUNT = 148
@@ -149,7 +152,8 @@ def oracle_step_rate(n_sample, seed=CFG):
 
 
 def workload_name():
-    return f"{CASE}_3d3v_{N_MODES}^3modes_{N_PER_GPU}particles_per_gpu_tol{TOL:g}_dt{DT}"
+    return (f"{CASE}_3d3v_{N_MODES}^3modes_{N_PER_GPU}particles_per_gpu_tol{TOL:g}_dt{DT}"
+            + ("_fp32" if CFG in FP32_CONFIGS else ""))
 
 
 # ------------------------------------------------------------- reference --
@@ -258,11 +262,14 @@ def run_ours(args, rank, world, local):
     n_global = N_PER_GPU * world
     stream = torch.cuda.current_stream(dev)
     sim = P.Simulation(P.physics(p.L, p.q_over_m, p.total_charge, p.B, p.A, p.c),
-                       P.propagator("pif", N_MODES, DT, tol=TOL), None, n_particles=n_global,
-                       device=local, rank=rank, world=world, space_size=world, nccl_id=nccl_id,
-                       stream=stream)
+                       P.propagator("pif", N_MODES, DT, tol=TOL, fp32=CFG in FP32_CONFIGS), None,
+                       n_particles=n_global, device=local, rank=rank, world=world, space_size=world,
+                       nccl_id=nccl_id, stream=stream)
     w, beta, n_up = sim.plan_info(0)
-    comm = sim.comm_info()
+    try:
+        comm = sim.comm_info()
+    except AttributeError:  # PIF_LIBRARY A/B build without pif_comm_info
+        comm = None
     xd = torch.from_numpy(x0).to(dev)
     vd = torch.from_numpy(v0).to(dev)
     sim.set_state(xd, vd)
@@ -340,7 +347,8 @@ def run_ours(args, rank, world, local):
             "metric": "particles pushed/s (PIF step)", "value": value, "unit": "particles/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "data": "synthetic",
+            "dtype": "f32 interpolation + f64" if CFG in FP32_CONFIGS else "f64",
             "config": {"workload": workload_name(), "n_particles_global": n_global,
                        "n_particles_per_gpu": n_local,
                        "modes": N_MODES, "nufft_tol": TOL, "es_width": w, "es_beta": beta,

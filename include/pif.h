@@ -75,6 +75,7 @@ typedef enum {
 
 typedef enum { PIF_PROP_PIF_NUFFT = 0, PIF_PROP_PIC_CIC = 1 } pif_prop_kind;
 #define PIF_FLAG_FP32_ALLREDUCE 1
+#define PIF_FLAG_FP32 2
 
 /* One propagator (fine F or coarse G of Sec. "Parareal for PIF"). */
 typedef struct {
@@ -87,7 +88,13 @@ typedef struct {
   int32_t flags;        /* bit 0 PIF_FLAG_FP32_ALLREDUCE: all-reduce the density (PIF rho_hat
                            box / PIC grid) over the space group in fp32 instead of fp64 --
                            halves the communication, the "single precision for the density
-                           field" of P:553-554 (meant for coarse propagators).  0 = default. */
+                           field" of P:553-554 (meant for coarse propagators).
+                           bit 1 PIF_FLAG_FP32: single-precision coarse propagator (P:553-554,
+                           "future work"): the type-2 interpolation (grid tile, kernel weights,
+                           accumulation) runs in fp32 on the vector pipe; positions, velocities,
+                           the push, the spread and the FFTs stay fp64.  PIF kind only, tol >=
+                           1e-5 (w <= 6; fp32 rounding ~1e-7 stays far inside 10 eps), else
+                           PIF_ERR_ARG.  0 = default. */
   double tol;           /* PIF: NUFFT tolerance eps in [1e-15, 1e-1); ignored for PIC */
   double dt;            /* timestep > 0 */
 } pif_propagator;

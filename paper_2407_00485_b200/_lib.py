@@ -22,6 +22,7 @@ lib = C.CDLL(_LIB_PATH)
 PIF_PROP_PIF_NUFFT = 0
 PIF_PROP_PIC_CIC = 1
 PIF_FLAG_FP32_ALLREDUCE = 1
+PIF_FLAG_FP32 = 2
 STATUS = {0: "PIF_OK", 1: "PIF_ERR_ARG", 2: "PIF_ERR_CONFIG", 3: "PIF_ERR_NUMERIC",
           4: "PIF_ERR_CUDA", 5: "PIF_ERR_NCCL", 6: "PIF_ERR_OOM", 7: "PIF_ERR_STATE"}
 
@@ -83,6 +84,8 @@ _sig = {
     "pif_profile_read": [_ctx, C.POINTER(C.c_double), C.c_int32, C.POINTER(_i64), C.c_int],
 }
 for _name, _args in _sig.items():
+    if os.environ.get("PIF_LIBRARY") and not hasattr(lib, _name):
+        continue  # A/B runs against an older build may lack newer exports
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = C.c_int
@@ -126,12 +129,12 @@ def physics(L, q_over_m, total_charge, B=(0.0, 0.0, 0.0), A=(0.0,) * 9, c=(0.0, 
     return p
 
 
-def propagator(kind, n, dt, tol=1e-12, spline_order=1, fp32_allreduce=False):
+def propagator(kind, n, dt, tol=1e-12, spline_order=1, fp32_allreduce=False, fp32=False):
     if isinstance(kind, str):
         kind = {"pif": PIF_PROP_PIF_NUFFT, "pic": PIF_PROP_PIC_CIC}[kind]
     p = PifPropagator()
     p.kind, p.n, p.spline_order, p.tol, p.dt = kind, n, spline_order, tol, dt
-    p.flags = PIF_FLAG_FP32_ALLREDUCE if fp32_allreduce else 0
+    p.flags = (PIF_FLAG_FP32_ALLREDUCE if fp32_allreduce else 0) | (PIF_FLAG_FP32 if fp32 else 0)
     return p
 
 

@@ -194,6 +194,9 @@ void horner_fit(int w, double beta, Horner& hc) {
 struct Plan {
   bool valid = false;
   bool fp32_ar = false;  // PIF_FLAG_FP32_ALLREDUCE
+  bool fp32 = false;     // PIF_FLAG_FP32: fp32 interpolation
+  bool simt = false;     // interpolation on the vector pipes (interp_simt.cu)
+  HornerF hcf{};
   void* ar32 = nullptr;  // fp32 staging buffer of the all-reduced density
   Horner hc{};
   int kind = 0, N = 0, order = 1;
@@ -238,7 +241,7 @@ struct pif_ctx_s {
   size_t ws_bytes = 0;
   double *xA = nullptr, *vA = nullptr, *xB = nullptr, *vB = nullptr;
   int *idA = nullptr, *idB = nullptr, *key = nullptr, *rnk = nullptr, *perm = nullptr, *counts = nullptr,
-      *offsets = nullptr, *flag = nullptr, *soff = nullptr, *ioff = nullptr, *moff = nullptr, *spart = nullptr;
+      *offsets = nullptr, *flag = nullptr, *ctr = nullptr, *soff = nullptr, *ioff = nullptr, *moff = nullptr, *spart = nullptr;
   int4 *sitems = nullptr, *iitems = nullptr, *iinfo = nullptr;
   int64_t max_s = 1, max_i = 1;
   double *partials = nullptr, *red = nullptr;
@@ -301,6 +304,7 @@ size_t layout(pif_ctx c, char* base) {
   take(c->iitems, max_i * sizeof(int4));
   take(c->iinfo, max_i * sizeof(int4));
   take(c->flag, 64);
+  take(c->ctr, 64);
   take(c->partials, 4 * kReduceBlocks * sizeof(double));
   take(c->red, 16 * sizeof(double));
   size_t fw = 0;
@@ -332,6 +336,7 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
   p.N = pr->n;
   p.order = pr->spline_order;
   p.fp32_ar = (pr->flags & PIF_FLAG_FP32_ALLREDUCE) != 0;
+  p.fp32 = (pr->flags & PIF_FLAG_FP32) != 0;
   p.tol = pr->tol;
   p.dt = pr->dt;
   const double L = c->ph.L;
@@ -393,6 +398,11 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     g.scale = n / L;
     g.beta = es_beta(w);
     horner_fit(w, g.beta, p.hc);
+    for (int k = 0; k < 16; ++k)
+      for (int j = 0; j <= kHornerDeg; ++j) p.hcf.a[k][j] = (float)p.hc.a[k][j];
+    // small widths: the per-particle vector kernel (w <= 5; w = 6 in fp32)
+    p.simt = simt_interp_supported(g) && (w <= 5 || p.fp32);
+    if (p.fp32 && !p.simt) return fail(PIF_ERR_ARG, "PIF_FLAG_FP32 needs tol >= 1e-5");
     p.n = n;
     p.nbricks = g.nkeys;
     c->max_bins = std::max(c->max_bins, p.nbricks);
@@ -420,7 +430,10 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
   CUFFT(cufftCreate(&p.inv));
   CUFFT(cufftSetAutoAllocation(p.inv, 0));
   int dims[3] = {n, n, n};
-  CUFFT(cufftMakePlanMany(p.inv, 3, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 3, &p.winv));
+  // fp32 plans: the three inverse transforms in single precision (C2R), whose
+  // float grids feed the fp32 interpolation directly
+  CUFFT(cufftMakePlanMany(p.inv, 3, dims, nullptr, 1, 0, nullptr, 1, 0, p.fp32 ? CUFFT_C2R : CUFFT_Z2D, 3,
+                          &p.winv));
   CUFFT(cufftSetStream(p.fwd, c->st));
   CUFFT(cufftSetStream(p.inv, c->st));
   p.valid = true;
@@ -434,13 +447,30 @@ pif_status validate_prop(const pif_propagator* pr) {
   if (pr->kind == PIF_PROP_PIF_NUFFT) {
     if (pr->n < 2 || pr->n % 2 || pr->n > 256) return fail(PIF_ERR_ARG, "PIF n must be even in [2, 256]");
     if (!(pr->tol >= 1e-15 && pr->tol < 1e-1)) return fail(PIF_ERR_ARG, "tol must be in [1e-15, 1e-1)");
+    if ((pr->flags & PIF_FLAG_FP32) && !(pr->tol >= 1e-5))
+      return fail(PIF_ERR_ARG, "PIF_FLAG_FP32 needs tol >= 1e-5");
   } else if (pr->kind == PIF_PROP_PIC_CIC) {
     if (pr->n < 4 || pr->n % 2 || pr->n > 512) return fail(PIF_ERR_ARG, "PIC n must be even in [4, 512]");
     if (pr->spline_order != 1) return fail(PIF_ERR_ARG, "PIC supports spline_order 1 (CIC) only");
+    if (pr->flags & PIF_FLAG_FP32) return fail(PIF_ERR_ARG, "PIF_FLAG_FP32 applies to PIF propagators");
   } else {
     return fail(PIF_ERR_ARG, "unknown propagator kind");
   }
   return PIF_OK;
+}
+
+// The three inverse transforms G3 -> grid3 (fp64, or fp32 for PIF_FLAG_FP32).
+cufftResult inverse_fft(const Plan& p) {
+  if (p.fp32) return cufftExecC2R(p.inv, (cufftComplex*)p.G3, (cufftReal*)p.grid3);
+  return cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3);
+}
+
+// Fused type-2 interpolation + push of plan p (tensor-core or vector kernel).
+cudaError_t interp_push(pif_ctx c, const Plan& p, double* x, double* v, int64_t stride, const int* id,
+                        double* Eout, const Sched& S, const PushArgs& P) {
+  if (p.simt)
+    return launch_interp_push_simt(p.grid3, x, v, stride, id, Eout, S, p.g, p.hc, p.hcf, p.fp32, P, c->st);
+  return launch_interp_push(p.grid3, x, v, stride, id, Eout, S, p.g, p.hc, P, c->st);
 }
 
 PushArgs push_args(pif_ctx c, const Plan& p, int kicks, int drift) {
@@ -498,7 +528,7 @@ pif_status ph_mark(pif_ctx c, int ph) {
 Sched sched_of(pif_ctx c, const Plan& p) {
   const int64_t M = keys_per_brick(p.g);
   return Sched{c->offsets, c->soff, c->ioff, c->moff, c->sitems, c->iitems, c->iinfo, c->spart, p.nbricks,
-               sched_max_s(p.nbricks, M, c->nloc), sched_max_i(p.nbricks, c->nloc)};
+               sched_max_s(p.nbricks, M, c->nloc), sched_max_i(p.nbricks, c->nloc), c->ctr};
 }
 
 // a0: counting sort of the working particles (xA, vA, idA) by brick of plan p.
@@ -545,10 +575,9 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_BOX, CU(launch_extract_box(p.spec, p.n, p.N, p.cor, c->q / (L * L * L), p.box, c->st)));
     if (c->space_size > 1)
       PH(PH_ALLREDUCE, TRY(density_allreduce(c, p, (double*)p.box, 2 * p.box_elems())));
-    PH(PH_POISSON, CU(launch_poisson_pad(p.box, p.n, p.N, L, p.cor, p.S, p.G3, c->st)));
-    PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
-    PH(PH_INTERP_PUSH, CU(launch_interp_push(p.grid3, c->xA, c->vA, n, c->idA, nullptr,
-                                             sched_of(c, p), p.g, p.hc, P, c->st)));
+    PH(PH_POISSON, CU(launch_poisson_pad(p.box, p.n, p.N, L, p.cor, p.S, p.G3, p.fp32, c->st)));
+    PH(PH_FFT_INV, CUFFT(inverse_fft(p)));
+    PH(PH_INTERP_PUSH, CU(interp_push(c, p, c->xA, c->vA, n, c->idA, nullptr, sched_of(c, p), P)));
     // own kernels: bin, schedule (reduce, partials, apply, fill), sort (index
     // scatter + gather), spread, extract, poisson, interp_push (cuFFT not counted)
     c->launches += 11;
@@ -1350,13 +1379,13 @@ static pif_status debug_sort(pif_ctx c, const Plan& p, DevBufs& B, const double*
   D.rk = D.id + 3 * n;
   D.perm = D.id + 4 * n;
   int* ib = nullptr;
-  const size_t ints = K + 5 * (K + 1) + sched_part_ints(K);
+  const size_t ints = K + 5 * (K + 1) + sched_part_ints(K) + 16;
   CU(B.alloc(&ib, ints * sizeof(int)));
   int4* items = nullptr;
   CU(B.alloc(&items, (ms + 2 * mi) * sizeof(int4)));
   D.counts = ib;
   D.S = Sched{ib + K, ib + 2 * K + 1, ib + 3 * K + 2, ib + 4 * K + 3, items, items + ms, items + ms + mi,
-              ib + 5 * K + 5, K, ms, mi};
+              ib + 5 * K + 5, K, ms, mi, ib + ints - 16};
   CU(cudaMemcpyAsync(D.x, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->st));
   if (s) CU(cudaMemcpyAsync(D.s, s, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
   CU(launch_iota(D.id, n, c->st));
@@ -1412,10 +1441,10 @@ pif_status pif_debug_type2(pif_ctx c, int which, const double* cin, const double
   CU(B.alloc(&E, 3 * n * sizeof(double)));
   CU(B.alloc(&dc, N3 * sizeof(double2)));
   CU(cudaMemcpyAsync(dc, cin, N3 * sizeof(double2), cudaMemcpyHostToDevice, c->st));
-  CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, c->st));
-  CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3));
+  CU(launch_debug_pad_KN(dc, p.n, p.N, p.cor, p.G3, p.fp32, c->st));
+  CUFFT(inverse_fft(p));
   PushArgs P = push_args(c, p, 0, 0);
-  CU(launch_interp_push(p.grid3, D.x2, nullptr, n, D.id2, E, D.S, p.g, p.hc, P, c->st));
+  CU(interp_push(c, p, D.x2, nullptr, n, D.id2, E, D.S, P));
   CU(cudaMemcpyAsync(out, E, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   TRY(sync_stream(c, c->st));
   return PIF_OK;

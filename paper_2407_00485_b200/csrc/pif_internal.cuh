@@ -5,6 +5,8 @@
 #include <cufft.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -58,6 +60,9 @@ struct Brick {
 constexpr int kHornerDeg = 14;
 struct Horner {
   double a[16][kHornerDeg + 1];  // a[k][j]: coefficient of s^j for node k
+};
+struct HornerF {  // the same coefficients rounded to fp32 (PIF_FLAG_FP32 interpolation)
+  float a[16][kHornerDeg + 1];
 };
 
 // Anchor cell of coordinate xs (grid units) with the window rule above; xs is
@@ -156,6 +161,7 @@ struct Sched {
   int4* iinfo;   // [max_i] decoded interp item: {bx, by, bz, sx | sy << 16}
   int* part;     // [sched_part_ints(nkeys)] scan scratch
   int64_t nkeys, max_s, max_i;
+  int* ctr;      // [16] work counters of the dynamically scheduled kernels (zeroed by their launchers)
 };
 // blocks of the schedule scan (kSchedT bricks each; >= 1)
 #ifndef PIF_SCHED_T
@@ -170,6 +176,31 @@ inline unsigned nblk_sched(int64_t nkeys, int64_t M) {
 inline size_t sched_part_ints(int64_t nkeys) { return 4 * ((size_t)nkeys / kSchedT + 2); }
 inline int64_t sched_max_s(int64_t nkeys, int64_t M, int64_t n) { return nkeys / M + n / kSpreadItem + 1; }
 inline int64_t sched_max_i(int64_t nkeys, int64_t n) { return nkeys + n / kInterpItem + 1; }
+
+// Per-device one-time launch setup: cudaFuncSetAttribute applies to the current
+// device only and the persistent grids are sized from its SM count, so the
+// result is cached per device (thread-safe).
+struct DevCache {
+  std::mutex mu;
+  int val[64] = {};
+};
+template <typename F>
+inline cudaError_t dev_cached(DevCache& dc, int& out, F&& init) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(dc.mu);
+  if (!dc.val[dev]) {
+    int v = 0;
+    e = init(dev, v);
+    if (e != cudaSuccess) return e;
+    if (v < 1) return cudaErrorInvalidConfiguration;
+    dc.val[dev] = v;
+  }
+  out = dc.val[dev];
+  return cudaSuccess;
+}
 
 // -------------------------------------------------------------- launchers --
 // All launchers enqueue on `st` and return cudaGetLastError().
@@ -191,14 +222,23 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
                                const int* id, double* Eout, const Sched& S, const Brick& g,
                                const Horner& hc, const PushArgs& P, cudaStream_t st);
+// Vector-pipe interpolation + push for small widths (interp_simt.cu): w <= 5
+// on the 8^3 / 6x6x8 tiles, w = 6 on 12^3; fp64 or fp32 (PIF_FLAG_FP32).
+bool simt_interp_supported(const Brick& g);
+// grid3: [3][n^3] double, or float for fp32 plans (single-precision inverse FFT).
+cudaError_t launch_interp_push_simt(const void* grid3, double* x, double* v, int64_t stride,
+                                    const int* id, double* Eout, const Sched& S, const Brick& g,
+                                    const Horner& hc, const HornerF& hcf, bool fp32, const PushArgs& P,
+                                    cudaStream_t st);
 cudaError_t launch_extract_box(const double2* spec, int n, int N, const double* cor, double scale,
                                double2* box, cudaStream_t st);
+// G3: 3 half spectra, double2 or (fp32) float2 for a single-precision inverse FFT.
 cudaError_t launch_poisson_pad(const double2* box, int n, int N, double L, const double* cor,
-                               const double* S, double2* G3, cudaStream_t st);
+                               const double* S, void* G3, bool fp32, cudaStream_t st);
 cudaError_t launch_debug_extract_KN(const double2* spec, int n, int N, const double* cor,
                                     double2* out, cudaStream_t st);
-cudaError_t launch_debug_pad_KN(const double2* c, int n, int N, const double* cor, double2* G3,
-                                cudaStream_t st);
+cudaError_t launch_debug_pad_KN(const double2* c, int n, int N, const double* cor, void* G3,
+                                bool fp32, cudaStream_t st);
 cudaError_t launch_field_energy(const double2* box, int N, double L, const double* S,
                                 double* out4, cudaStream_t st);
 cudaError_t launch_particle_moments(const double* v, int64_t stride, int64_t n, double* partials,

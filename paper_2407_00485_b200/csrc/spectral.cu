@@ -12,6 +12,12 @@
 
 namespace pif {
 
+template <typename C2>
+__device__ __forceinline__ C2 cplx(double re, double im) {
+  if constexpr (sizeof(C2) == 8) return make_float2((float)re, (float)im);
+  else return make_double2(re, im);
+}
+
 __device__ __forceinline__ int64_t spec_index(int mx, int my, int mz, int n) {
   int ix = mx < 0 ? mx + n : mx;
   int iy = my < 0 ? my + n : my;
@@ -43,9 +49,10 @@ __device__ __forceinline__ double completion_weight(int mx, int my, int mz, int 
 
 // G_d[k] = omega_k S_k E_{d,k} / psi^(k), E_{d,k} = -i k_d S_k rho_tilde_k / |k|^2,
 // k = 0 -> 0 (eq. gather_pif); zero outside the box.
+template <typename C2>
 __global__ void k_poisson_pad(const double2* __restrict__ box, int n, int N, double L,
                               const double* __restrict__ cor, const double* __restrict__ S,
-                              double2* __restrict__ G3) {
+                              C2* __restrict__ G3) {
   const int H = N / 2, NB = N + 1, NZ = H + 1, nz = n / 2 + 1;
   const int64_t tot = (int64_t)n * n * nz;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -70,9 +77,9 @@ __global__ void k_poisson_pad(const double2* __restrict__ box, int n, int N, dou
     g1 = make_double2(f * ky * r.y, -f * ky * r.x);
     g2 = make_double2(f * kz * r.y, -f * kz * r.x);
   }
-  G3[i] = g0;
-  G3[tot + i] = g1;
-  G3[2 * tot + i] = g2;
+  G3[i] = cplx<C2>(g0.x, g0.y);
+  G3[tot + i] = cplx<C2>(g1.x, g1.y);
+  G3[2 * tot + i] = cplx<C2>(g2.x, g2.y);
 }
 
 // Debug type-1 output on K_N in (mx, my, mz) row-major order, no scale.
@@ -100,8 +107,9 @@ __global__ void k_debug_extract_KN(const double2* __restrict__ spec, int n, int 
 
 // Debug type-2 input: c on K_N -> G (component 0) = c^box / psi^ on the half
 // spectrum, c^box_k = (c_k 1[k in K_N] + conj(c_{-k}) 1[-k in K_N]) / 2 (R2).
+template <typename C2>
 __global__ void k_debug_pad_KN(const double2* __restrict__ c, int n, int N,
-                               const double* __restrict__ cor, double2* __restrict__ G3) {
+                               const double* __restrict__ cor, C2* __restrict__ G3) {
   const int H = N / 2, nz = n / 2 + 1;
   const int64_t tot = (int64_t)n * n * nz;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -128,9 +136,9 @@ __global__ void k_debug_pad_KN(const double2* __restrict__ c, int n, int N,
     double f = 0.5 * cor[mx + H] * cor[my + H] * cor[mz + H];
     g = make_double2(re * f, im * f);
   }
-  G3[i] = g;
-  G3[tot + i] = make_double2(0.0, 0.0);
-  G3[2 * tot + i] = make_double2(0.0, 0.0);
+  G3[i] = cplx<C2>(g.x, g.y);
+  G3[tot + i] = cplx<C2>(0.0, 0.0);
+  G3[2 * tot + i] = cplx<C2>(0.0, 0.0);
 }
 
 // W_d = (L^3/2) sum_{K_N} |E_{d,k}|^2 = (L^3/2) sum_box omega_k |E_{d,k}|^2, the box
@@ -285,9 +293,10 @@ cudaError_t launch_extract_box(const double2* spec, int n, int N, const double* 
   return cudaGetLastError();
 }
 cudaError_t launch_poisson_pad(const double2* box, int n, int N, double L, const double* cor,
-                               const double* S, double2* G3, cudaStream_t st) {
+                               const double* S, void* G3, bool fp32, cudaStream_t st) {
   int64_t tot = (int64_t)n * n * (n / 2 + 1);
-  k_poisson_pad<<<nblk(tot, 256), 256, 0, st>>>(box, n, N, L, cor, S, G3);
+  if (fp32) k_poisson_pad<<<nblk(tot, 256), 256, 0, st>>>(box, n, N, L, cor, S, (float2*)G3);
+  else k_poisson_pad<<<nblk(tot, 256), 256, 0, st>>>(box, n, N, L, cor, S, (double2*)G3);
   return cudaGetLastError();
 }
 cudaError_t launch_debug_extract_KN(const double2* spec, int n, int N, const double* cor,
@@ -296,10 +305,11 @@ cudaError_t launch_debug_extract_KN(const double2* spec, int n, int N, const dou
   k_debug_extract_KN<<<nblk(tot, 256), 256, 0, st>>>(spec, n, N, cor, out);
   return cudaGetLastError();
 }
-cudaError_t launch_debug_pad_KN(const double2* c, int n, int N, const double* cor, double2* G3,
-                                cudaStream_t st) {
+cudaError_t launch_debug_pad_KN(const double2* c, int n, int N, const double* cor, void* G3,
+                                bool fp32, cudaStream_t st) {
   int64_t tot = (int64_t)n * n * (n / 2 + 1);
-  k_debug_pad_KN<<<nblk(tot, 256), 256, 0, st>>>(c, n, N, cor, G3);
+  if (fp32) k_debug_pad_KN<<<nblk(tot, 256), 256, 0, st>>>(c, n, N, cor, (float2*)G3);
+  else k_debug_pad_KN<<<nblk(tot, 256), 256, 0, st>>>(c, n, N, cor, (double2*)G3);
   return cudaGetLastError();
 }
 cudaError_t launch_field_energy(const double2* box, int N, double L, const double* S,

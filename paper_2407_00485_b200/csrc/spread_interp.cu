@@ -25,36 +25,10 @@
 //
 // Fragment layouts of m8n8k4.f64 (lane l, g = l >> 2, t = l & 3):
 //   A (8x4, row): A[g][t];  B (4x8, col): B[t][g];  C (8x8): C[g][2t], C[g][2t+1].
-#include <mutex>
-
 #include "pif_internal.cuh"
 
 namespace pif {
 
-// Per-device one-time launch setup: cudaFuncSetAttribute applies to the current
-// device only and the persistent grids are sized from its SM count, so the
-// result is cached per device (thread-safe).
-struct DevCache {
-  std::mutex mu;
-  int val[64] = {};
-};
-template <typename F>
-static cudaError_t dev_cached(DevCache& dc, int& out, F&& init) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  std::lock_guard<std::mutex> lk(dc.mu);
-  if (!dc.val[dev]) {
-    int v = 0;
-    e = init(dev, v);
-    if (e != cudaSuccess) return e;
-    if (v < 1) return cudaErrorInvalidConfiguration;
-    dc.val[dev] = v;
-  }
-  out = dc.val[dev];
-  return cudaSuccess;
-}
 
 #ifndef PIF_SPREAD_MINB
 #define PIF_SPREAD_MINB 3  // 3 CTAs/SM (shared memory allows 3 for the 16^3 tile)
@@ -142,11 +116,8 @@ struct Psi {
 
 // Decode a work item: spread (sub == false) = {brick, start, end}; interpolation
 // (sub == true) = {sub-brick key, start, end}; returns false past the last item.
-__device__ __forceinline__ bool tile_of(const Brick& g, const Sched& S, bool sub, int T0[3],
-                                        int64_t& start, int64_t& end) {
-  const int64_t item = blockIdx.x;
-  const int total = sub ? S.ioff[S.nkeys] : S.soff[S.nkeys];
-  if (item >= total) return false;
+__device__ __forceinline__ bool tile_of(const Brick& g, const Sched& S, bool sub, int64_t item,
+                                        int T0[3], int64_t& start, int64_t& end) {
   const int4 it = sub ? S.iitems[item] : S.sitems[item];
   start = it.y;
   end = it.z;
@@ -295,6 +266,9 @@ struct SpreadCfg {
   static constexpr int NW = NCT / CT;             // warps
   static constexpr int ZT = (RZ + 7) / 8;         // z tiles of 8 (psi_z rows zero-padded)
   static constexpr bool PADC = NCT * 8 != RX * RY;  // padded columns c >= RX RY (A = 0: py rows >= RY)
+  // resident CTAs per SM the register budget must allow: small tiles (5 warps)
+  // fit 5 by shared memory, and the register allocation decides between 3 and 4
+  static constexpr int MINB = NW <= 5 ? 4 : PIF_SPREAD_MINB;
   static_assert(RY + spread_pad_rows(RX, RY) <= RowStride<RY>::v, "py row stride");
   static_assert(NCT % CT == 0, "tile shape");
 };
@@ -303,26 +277,35 @@ struct SpreadCfg {
 // instead of per brick (tile RS): fewer padded FMAs per particle, more
 // REDG.ADD.F64 per particle in the flush.
 template <int RX, int RY, int RZ, bool HAS_S, bool SUB>
-__global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, PIF_SPREAD_MINB)
+__global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, SpreadCfg<RX, RY, RZ>::MINB)
     k_spread(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
              double s_uniform, const Sched Sc, Brick g,
              const __grid_constant__ Horner hc, double* __restrict__ grid) {
   using C = SpreadCfg<RX, RY, RZ>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Psi<RX, RY, RZ>& sm = *reinterpret_cast<Psi<RX, RY, RZ>*>(smem_raw);
+  const int total = SUB ? Sc.ioff[Sc.nkeys] : Sc.soff[Sc.nkeys];
+  // dynamically scheduled items: the first gridDim.x by block index, the rest
+  // from the work counter Sc.ctr[0] (the grid is sized from the occupancy; crowded
+  // and empty bricks differ by orders of magnitude in cost)
+  __shared__ int next_item;
+  for (int item = blockIdx.x; item < total;) {
+  // claim the next item now: the counter's round trip overlaps this item
+  int claimed = 0;
+  if (threadIdx.x == 0) claimed = gridDim.x + atomicAdd(Sc.ctr, 1);
+  do {  // one item (break: empty item)
   int T0[3];
   int64_t start, end;
   if (SUB) {
-    if ((int)blockIdx.x >= Sc.ioff[Sc.nkeys]) return;
-    const int4 e = Sc.iitems[blockIdx.x];
-    const int4 f = Sc.iinfo[blockIdx.x];  // {bx, by, bz, sx | sy << 16}
+    const int4 e = Sc.iitems[item];
+    const int4 f = Sc.iinfo[item];  // {bx, by, bz, sx | sy << 16}
     start = e.y;
     end = e.z;
     T0[0] = f.x * g.sb[0] - g.hw + (f.w & 0xffff) * g.ib[0];
     T0[1] = f.y * g.sb[1] - g.hw + (f.w >> 16) * g.ib[1];
     T0[2] = f.z * g.sb[2] - g.hw;
-    if (start >= end) return;
-  } else if (!tile_of(g, Sc, false, T0, start, end)) return;
+    if (start >= end) break;
+  } else if (!tile_of(g, Sc, false, item, T0, start, end)) break;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gr = lane >> 2, tq = lane & 3;
   // A-fragment rows: column c = (wid*CT + ct)*8 + gr
@@ -379,6 +362,12 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, PIF_SPREAD_MIN
         if (z < RZ && val != 0.0 && (!C::PADC || acy[ct] < RY))
           atomicAdd(colp + wrapi(T0[2] + z, n), val * s_uniform);
       }
+  }
+  } while (0);
+  if (threadIdx.x == 0) next_item = claimed;
+  __syncthreads();
+  item = next_item;
+  __syncthreads();
   }
 }
 
@@ -1062,17 +1051,29 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
   const int T = 32 * SpreadCfg<A, B, Cz>::NW;
   const size_t smem = sizeof(Psi<A, B, Cz, kChunk>);
   static DevCache cache;
-  int ok = 0;
-  cudaError_t e = dev_cached(cache, ok, [&](int, int& v) {
+  int ctas = 0;  // resident CTAs on the device
+  cudaError_t e = dev_cached(cache, ctas, [&](int dev, int& v) {
+    int sms = 0, per = 0;
     cudaError_t r = cudaFuncSetAttribute(k_spread<A, B, Cz, true, SUB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (r == cudaSuccess)
       r = cudaFuncSetAttribute(k_spread<A, B, Cz, false, SUB>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    v = 1;
+    if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (r == cudaSuccess)
+      r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_spread<A, B, Cz, false, SUB>, T, smem);
+    v = sms * per;
     return r;
   });
   if (e != cudaSuccess) return e;
+  // an item bound of up to ~n_keys CTAs (most of them empty) -> 2 waves of
+  // resident CTAs striding over the items
+#ifndef PIF_SPREAD_WAVES
+#define PIF_SPREAD_WAVES 2
+#endif
+  if ((int64_t)nbr > PIF_SPREAD_WAVES * (int64_t)ctas) nbr = PIF_SPREAD_WAVES * ctas;
+  cudaError_t e0 = cudaMemsetAsync(offsets.ctr, 0, sizeof(int), st);
+  if (e0 != cudaSuccess) return e0;
   if (s)
     k_spread<A, B, Cz, true, SUB><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
   else

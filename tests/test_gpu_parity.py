@@ -423,8 +423,8 @@ def test_crowded_bricks_item_splitting():
     cells = np.floor(x / h).astype(int)
     sub = cells // np.array([2, 2, 4])[:, None]   # interpolation sub-bricks (2x2x4 cells)
     brk = cells // 4                               # spreading bricks (4^3 cells)
-    assert np.unique(sub, axis=1, return_counts=True)[1].max() > 4 * 1024
-    assert np.unique(brk, axis=1, return_counts=True)[1].max() > 4 * 4096
+    assert np.unique(sub, axis=1, return_counts=True)[1].max() > 2 * 1024
+    assert np.unique(brk, axis=1, return_counts=True)[1].max() > 2 * 4096
     sim = sim_for(phys, P.propagator("pif", N, 0.003125, tol=tol), n=n)
     assert sim.plan_info(0)[2] == 32
     s = np.random.default_rng(22).standard_normal(n)
@@ -503,3 +503,42 @@ def test_set_state_wraps_positions_outside_the_box():
     assert np.abs(O.min_image(a[0] - b[0], phys.L)).max() <= 1e-13 * phys.L
     assert np.abs(a[1] - b[1]).max() <= 1e-13 * np.abs(a[1]).max()
     assert np.all((b[0] >= 0) & (b[0] < phys.L))
+
+
+# ------------------------------------------ f3: fp32 coarse propagator ------
+@pytest.mark.parametrize("tol", [1e-4, 1e-5])
+@pytest.mark.parametrize("npart", [16384, 16 * 16 ** 3 + 3])  # sparse 8^3 tile / dense 6x6x8 (w = 5)
+def test_fp32_type2_vs_nudft(tol, npart):
+    """PIF_FLAG_FP32: the fp32 interpolation is within 10 eps of the
+    exact NUDFT (fp32 rounding ~1e-7 relative << 10 eps for eps >= 1e-5)."""
+    phys = landau_physics()
+    x, _ = landau_state(npart, 51)
+    rng = np.random.default_rng(52)
+    c = rng.standard_normal((8, 8, 8)) + 1j * rng.standard_normal((8, 8, 8))
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=tol, fp32=True), n=npart)
+    got = P.pif_debug_type2(sim.ctx, 0, c, x)
+    ref = O.nudft_type2(c, x, 8, phys.L)
+    err = rel_l2(got, ref)
+    assert err <= 10 * tol
+    assert err > 1e-9  # it really ran in single precision
+
+
+def test_fp32_coarse_steps_vs_oracle():
+    """5 steps of the fp32 coarse propagator (eps_g = 1e-4, dense w = 5 tile) vs
+    the exact oracle, with the bound of test_dense_tiles_steps_vs_oracle
+    (2 x 10 eps on the field-driven velocity change and displacement)."""
+    phys = landau_physics()
+    n, N, dt, K, tol = 16 * 16 ** 3, 8, 0.05, 5, 1e-4
+    x0, v0 = landau_state(n, 53)
+    x, v, *_ = run_gpu(phys, P.propagator("pif", N, dt, tol=tol, fp32=True), x0, v0, K)
+    xr, vr = O.run(x0, v0, K, O.Propagator("pif", N, dt), O.PhysicsParams.from_inputs(phys))
+    assert np.linalg.norm(v - vr) <= 2 * 10 * tol * np.linalg.norm(vr - v0)
+    disp_ref = O.min_image(xr - (x0 + K * dt * v0), phys.L)
+    assert np.linalg.norm(O.min_image(x - xr, phys.L)) <= 2 * 10 * tol * np.linalg.norm(disp_ref)
+
+
+def test_fp32_flag_rejected_below_1e5():
+    phys = landau_physics()
+    with pytest.raises(P.PifError) as e:
+        sim_for(phys, P.propagator("pif", 8, 0.05, tol=1e-7, fp32=True), n=100)
+    assert e.value.status == 1
