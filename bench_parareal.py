@@ -1,16 +1,23 @@
 #!/usr/bin/env python
-"""Parareal speedup vs serial time stepping (BASELINE.json metric, second half;
-configs[4] family: Landau damping, 64^3 modes, coarse = PIF eps 1e-4 or
-CIC-PIC 32^3, both with temporal coarsening Delta t_g = 0.05).
+"""Parareal speedup (BASELINE.json metric, second half; configs[4] family:
+Landau damping, 64^3 modes, coarse = PIF eps 1e-4 (fp64 or fp32) or CIC-PIC
+32^3, both with temporal coarsening Delta t_g = 0.05).
 
-  torchrun --nproc-per-node N bench_parareal.py [--coarse pif|pic] [--particles P]
+  torchrun --nproc-per-node N bench_parareal.py [--coarse pif|pif32|pic]
+           [--particles P] [--space S]
 
-One parareal slice per GPU (time_size = N, space_size = 1).  Rank 0 first runs
-the serial fine propagator over [0, T] alone (the "serial time stepping"
-reference of P:716-718), then all ranks run pif_parareal; speedup =
-t_serial / t_parareal (t_parareal = max over ranks of the pif_parareal call,
-from the start of the coarse sweep to the last slice's retirement).  Reading
-R21 of DESIGN.md: T = 2.4, Delta t_f = 0.003125, eps_f = 1e-7, stop tol 1e-8.
+Rank layout: N = S x T ranks, T = N / S parareal slices, each slice particle-
+decomposed over S GPUs (space x time, PAPER.md:139-141 with P:151-173).
+Two references (reading c20 of SURVEY.md 8c; PAPER.md:534-535 compares with
+"spatial parallelization alone", P:716-718 with serial time stepping):
+  t_serial -- the fine propagator over [0, T] on 1 GPU (rank 0 alone);
+  t_space  -- the fine propagator over [0, T] particle-decomposed over all N
+              GPUs (max over ranks);
+then all ranks run pif_parareal: t_parareal = max over ranks of the call, from
+the start of the coarse sweep to the last slice's retirement.  Per-rank phase
+times (coarse sweep, fine, coarse, communication wait, total) are all-gathered.
+Reading R21 of DESIGN.md: T = 2.4, Delta t_f = 0.003125, eps_f = 1e-7, stop
+tol 1e-8.
 """
 from __future__ import annotations
 
@@ -26,7 +33,9 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--coarse", default="pif", choices=["pif", "pic"])
+    ap.add_argument("--coarse", default="pif", choices=["pif", "pif32", "pic"])
+    ap.add_argument("--space", type=int, default=1, help="GPUs per slice (space_size)")
+    ap.add_argument("--no-space-ref", action="store_true")
     ap.add_argument("--particles", type=int, default=1 << 22)
     ap.add_argument("--modes", type=int, default=64)
     ap.add_argument("--T", type=float, default=2.4)
@@ -59,13 +68,15 @@ def main():
     p = landau_physics()
     phys = P.physics(p.L, p.q_over_m, p.total_charge)
     fine = P.propagator("pif", args.modes, args.dtf, tol=args.tolf)
-    coarse = (P.propagator("pif", args.modes, args.dtg, tol=args.tolg) if args.coarse == "pif"
-              else P.propagator("pic", 32, args.dtg))
+    coarse = (P.propagator("pic", 32, args.dtg) if args.coarse == "pic" else
+              P.propagator("pif", args.modes, args.dtg, tol=args.tolg, fp32=args.coarse == "pif32"))
+    S = args.space
+    assert world % S == 0, "--space must divide the number of ranks"
     n = args.particles
     x0, v0 = landau_state(n, 4)
     xd, vd = torch.from_numpy(x0).to(dev), torch.from_numpy(v0).to(dev)
     nsteps = int(round(args.T / args.dtf))
-    slices = max(world, 1)
+    slices = max(world // S, 1)
     max_iter = args.max_iter or slices
 
     t_serial = None
@@ -85,8 +96,33 @@ def main():
     if world > 1:
         dist.barrier()
 
+    # spatial parallelization alone: the fine propagator particle-decomposed
+    # over all ranks (one rho_hat all-reduce per step)
+    t_space = None
+    if world > 1 and not args.no_space_ref:
+        sp = P.Simulation(phys, fine, None, n_particles=n, device=local, rank=rank, world=world,
+                          space_size=world, nccl_id=nid)
+        a, c = sp.first, sp.n_local
+        xa, va = xd[:, a:a + c].contiguous(), vd[:, a:a + c].contiguous()
+        sp.set_state(xa, va)
+        sp.step(3)
+        sp.set_state(xa, va)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sp.step(nsteps)
+        sp.get_state()
+        torch.cuda.synchronize()
+        tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_space = float(tt.item())
+        sp.close()
+        del xa, va
+
     sim = P.Simulation(phys, fine, coarse, n_particles=n, device=local, rank=rank, world=world,
-                       space_size=1, nccl_id=nid)
+                       space_size=S, nccl_id=nid)
+    a, c = sim.first, sim.n_local
+    xd, vd = xd[:, a:a + c].contiguous(), vd[:, a:a + c].contiguous()
     # untimed warm-up (lazy module loading, first cuFFT executions on every rank)
     sim.set_state(xd, vd)
     sim.parareal(0.0, slices * args.dtg, slices, 1, args.stop)
@@ -100,17 +136,32 @@ def main():
     el = time.perf_counter() - t0
     xp, vp = sim.get_state()
     tt = torch.tensor([el], dtype=torch.float64, device=dev)
+    phases = torch.tensor([rep[k] for k in ("t_coarse0", "t_fine", "t_coarse", "t_comm", "t_total")]
+                          + [el], dtype=torch.float64, device=dev)
+    per_rank = [phases]
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        # final state of the last slice -> rank 0
-        if rank == world - 1:
+        per_rank = [torch.empty_like(phases) for _ in range(world)]
+        dist.all_gather(per_rank, phases)
+        # final state of the last slice (space ranks (T-1) S .. T S - 1) -> rank 0
+        last = list(range((slices - 1) * S, slices * S))
+        if rank in last and rank != 0:
             dist.send(xp, 0)
             dist.send(vp, 0)
         if rank == 0:
-            xp = torch.empty_like(xp)
-            vp = torch.empty_like(vp)
-            dist.recv(xp, world - 1)
-            dist.recv(vp, world - 1)
+            parts_x, parts_v = [], []
+            for r in last:
+                cnt = P.pif_partition(n, S, r - (slices - 1) * S)[1]
+                if r == 0:
+                    bx, bv = xp, vp
+                else:
+                    bx = torch.empty((3, cnt), dtype=torch.float64, device=dev)
+                    bv = torch.empty_like(bx)
+                    dist.recv(bx, r)
+                    dist.recv(bv, r)
+                parts_x.append(bx)
+                parts_v.append(bv)
+            xp, vp = torch.cat(parts_x, dim=1), torch.cat(parts_v, dim=1)
     t_par = float(tt.item())
     if rank == 0:
         L = p.L
@@ -119,15 +170,20 @@ def main():
         line = {
             "metric": "parareal speedup vs serial (PIF fine)", "value": t_serial / t_par,
             "unit": "x", "n_gpus": world, "higher_is_better": True,
-            "t_serial_s": t_serial, "t_parareal_s": t_par, "iterations": rep["iterations"],
+            "speedup_vs_space_only": (t_space / t_par) if t_space else None,
+            "space_only_speedup_vs_serial": (t_serial / t_space) if t_space else None,
+            "t_serial_s": t_serial, "t_space_only_s": t_space, "t_parareal_s": t_par,
+            "layout": {"space": S, "time": slices}, "iterations": rep["iterations"],
             "converged": rep["converged"], "retired_at": rep["retired_at"],
             "max_rel_err_x_vs_serial": float(np.abs(dx).max() / L),
             "max_rel_err_v_vs_serial": float((vp - vs).abs().max().item() / vs.abs().max().item()),
-            "phase_s_rank0": {k: rep[k] for k in ("t_coarse0", "t_fine", "t_coarse", "t_comm")},
+            "phase_s_per_rank": [dict(zip(("t_coarse0", "t_fine", "t_coarse", "t_comm", "t_total",
+                                           "t_call"), [round(float(v), 4) for v in t.tolist()]))
+                                 for t in per_rank],
             "push_rate_parareal": n * nsteps / t_par, "push_rate_serial": n * nsteps / t_serial,
             "config": {"workload": "landau_3d3v", "modes": args.modes, "n_particles": n, "T": args.T,
                        "dt_f": args.dtf, "eps_f": args.tolf, "coarse": args.coarse,
-                       "dt_g": args.dtg, "eps_g": args.tolg if args.coarse == "pif" else None,
+                       "dt_g": args.dtg, "eps_g": args.tolg if args.coarse != "pic" else None,
                        "pic_grid": 32 if args.coarse == "pic" else None, "stop_tol": args.stop,
                        "slices": slices, "fine_steps": nsteps},
         }

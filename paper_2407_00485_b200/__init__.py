@@ -9,6 +9,7 @@ from __future__ import annotations
 from ._lib import (PIF_PROP_PIC_CIC, PIF_PROP_PIF_NUFFT, PifError, lib, physics,  # noqa: F401
                    pif_debug_push, pif_debug_type1, pif_debug_type2, pif_field_energy,
                    pif_finalize, pif_get_rho, pif_get_state, pif_init, pif_local_count, pif_nccl_unique_id,
+                   pif_partition,
                    pif_comm_info, pif_parareal, pif_plan_info, pif_profile, pif_profile_read, pif_set_state, pif_set_workspace, pif_step,
                    pif_workspace_size, propagator)
 
