@@ -47,8 +47,10 @@ CONFIGS = {1: ("landau", 32, 1 << 21, 1e-12, 0.05),     # C2
            6: ("landau", 64, 1 << 22, 1e-4, 0.05),        # C5-reduced parareal coarse (PIF) propagator
            7: ("landau", 64, 1 << 26, 1e-4, 0.05),        # C5 coarse (PIF, eps 1e-4) propagator (1 GPU)
            8: ("landau", 64, 1 << 26, 1e-4, 0.05),        # C5 coarse propagator in fp32 (PIF_FLAG_FP32)
-           9: ("landau", 64, 1 << 22, 1e-4, 0.05)}        # C5-reduced coarse propagator in fp32
+           9: ("landau", 64, 1 << 22, 1e-4, 0.05),        # C5-reduced coarse propagator in fp32
+           10: ("landau", 32, 1 << 26, 0.0, 0.05)}        # C5 coarse G_B: CIC-PIC on a 32^3 grid
 FP32_CONFIGS = (8, 9)
+PIC_CONFIGS = (10,)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 SM_COUNT = 148
@@ -152,6 +154,8 @@ def oracle_step_rate(n_sample, seed=CFG):
 
 
 def workload_name():
+    if CFG in PIC_CONFIGS:
+        return f"{CASE}_3d3v_cic-pic_{N_MODES}^3grid_{N_PER_GPU}particles_per_gpu_dt{DT}"
     return (f"{CASE}_3d3v_{N_MODES}^3modes_{N_PER_GPU}particles_per_gpu_tol{TOL:g}_dt{DT}"
             + ("_fp32" if CFG in FP32_CONFIGS else ""))
 
@@ -262,6 +266,7 @@ def run_ours(args, rank, world, local):
     n_global = N_PER_GPU * world
     stream = torch.cuda.current_stream(dev)
     sim = P.Simulation(P.physics(p.L, p.q_over_m, p.total_charge, p.B, p.A, p.c),
+                       P.propagator("pic", N_MODES, DT) if CFG in PIC_CONFIGS else
                        P.propagator("pif", N_MODES, DT, tol=TOL, fp32=CFG in FP32_CONFIGS), None,
                        n_particles=n_global, device=local, rank=rank, world=world, space_size=world,
                        nccl_id=nccl_id, stream=stream)
@@ -284,25 +289,36 @@ def run_ours(args, rank, world, local):
     value = n_global * args.steps / (total_ms / 1000.0)
 
     # roofline of the dominant kernel (per launch; one launch per step)
-    dom = max(("spread", "interp_push"), key=lambda k: phases[k])
-    # tensor-product work (spread 2w^3, interpolation 3 x 2w^3 flops)
-    # plus the kernel evaluation of one transform, 3 dims x w nodes x a degree-(w+3)
-    # Horner polynomial = 6w(w+3) flops
-    flops_per_particle = {"spread": 2 * w ** 3, "interp_push": 6 * w ** 3}[dom] + 6 * w * (w + 3)
+    dom = max(("spread", "interp_push", "pic_deposit", "pic_gather_push"), key=lambda k: phases[k])
     launch_s = phases[dom] / args.steps / 1000.0
-    achieved = sim.n_local * flops_per_particle / launch_s / 1e12
     sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peak = SM_COUNT * FP64_FMA_PER_SM_CLK * 2 * sm_max * 1e6 / 1e12
-    traffic = None
-    if os.path.exists(TRAFFIC_FILE):
-        try:
-            traffic = json.load(open(TRAFFIC_FILE)).get(dom)
-        except Exception:
-            traffic = None
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": dom,
-                "algorithmic": f"{flops_per_particle} FP64 flops/particle (w={w}: tensor product + ES kernel evaluation, SURVEY 8(d)) x {sim.n_local} particles per launch",
-                "peak_source": f"derived FP64: {SM_COUNT} SMs x {FP64_FMA_PER_SM_CLK} DFMA/clk x 2 x {sm_max:.0f} MHz"}
+    if dom.startswith("pic"):
+        # CIC-PIC kernels are HBM-bound: the deposit reads x (24 B/particle), the
+        # gather + push reads and writes x, v (96 B/particle) -- SURVEY 8(d)
+        bpp = 24 if dom == "pic_deposit" else 96
+        achieved = sim.n_local * bpp / launch_s / 1e9
+        peak = json.load(open(PEAKS_FILE)).get("hbm_gbs", 6542.7) if os.path.exists(PEAKS_FILE) else 6542.7
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "kernel": dom,
+                    "algorithmic": f"{bpp} B/particle x {sim.n_local} particles per launch",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        # tensor-product work (spread 2w^3, interpolation 3 x 2w^3
+        # flops) plus the kernel evaluation of one transform, 3 dims x w nodes x a
+        # degree-(w+3) Horner polynomial = 6w(w+3) flops
+        flops_per_particle = {"spread": 2 * w ** 3, "interp_push": 6 * w ** 3}[dom] + 6 * w * (w + 3)
+        achieved = sim.n_local * flops_per_particle / launch_s / 1e12
+        peak = SM_COUNT * FP64_FMA_PER_SM_CLK * 2 * sm_max * 1e6 / 1e12
+        traffic = None
+        if os.path.exists(TRAFFIC_FILE):
+            try:
+                traffic = json.load(open(TRAFFIC_FILE)).get(dom)
+            except Exception:
+                traffic = None
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic, "kernel": dom,
+                    "algorithmic": f"{flops_per_particle} FP64 flops/particle (w={w}: tensor product + ES kernel evaluation, SURVEY 8(d)) x {sim.n_local} particles per launch",
+                    "peak_source": f"derived FP64: {SM_COUNT} SMs x {FP64_FMA_PER_SM_CLK} DFMA/clk x 2 x {sm_max:.0f} MHz"}
 
     # end-to-end through the public API with host (pinned) buffers
     e2e = None

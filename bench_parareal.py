@@ -60,11 +60,13 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    nid = None
-    if world > 1:
+    def new_id():
+        """A fresh ncclUniqueId from rank 0 (one per communicator initialisation)."""
+        if world == 1:
+            return None
         obj = [P.pif_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
+        return obj[0]
     p = landau_physics()
     phys = P.physics(p.L, p.q_over_m, p.total_charge)
     fine = P.propagator("pif", args.modes, args.dtf, tol=args.tolf)
@@ -79,6 +81,11 @@ def main():
     slices = max(world // S, 1)
     max_iter = args.max_iter or slices
 
+    clk = None
+    if rank == 0:  # clocks and throttle reasons of this GPU during the whole run
+        from bench import ClockSampler
+        clk = ClockSampler(local)
+        clk.start()
     t_serial = None
     xs = None
     if rank == 0:
@@ -101,7 +108,7 @@ def main():
     t_space = None
     if world > 1 and not args.no_space_ref:
         sp = P.Simulation(phys, fine, None, n_particles=n, device=local, rank=rank, world=world,
-                          space_size=world, nccl_id=nid)
+                          space_size=world, nccl_id=new_id())
         a, c = sp.first, sp.n_local
         xa, va = xd[:, a:a + c].contiguous(), vd[:, a:a + c].contiguous()
         sp.set_state(xa, va)
@@ -120,7 +127,7 @@ def main():
         del xa, va
 
     sim = P.Simulation(phys, fine, coarse, n_particles=n, device=local, rank=rank, world=world,
-                       space_size=S, nccl_id=nid)
+                       space_size=S, nccl_id=new_id())
     a, c = sim.first, sim.n_local
     xd, vd = xd[:, a:a + c].contiguous(), vd[:, a:a + c].contiguous()
     # untimed warm-up (lazy module loading, first cuFFT executions on every rank)
@@ -181,6 +188,7 @@ def main():
                                            "t_call"), [round(float(v), 4) for v in t.tolist()]))
                                  for t in per_rank],
             "push_rate_parareal": n * nsteps / t_par, "push_rate_serial": n * nsteps / t_serial,
+            "clocks_rank0": clk.stop() if clk else None,
             "config": {"workload": "landau_3d3v", "modes": args.modes, "n_particles": n, "T": args.T,
                        "dt_f": args.dtf, "eps_f": args.tolf, "coarse": args.coarse,
                        "dt_g": args.dtg, "eps_g": args.tolg if args.coarse != "pic" else None,

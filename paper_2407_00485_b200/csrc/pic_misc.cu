@@ -36,12 +36,64 @@ __global__ void k_cic_deposit(const double* __restrict__ x, int64_t stride, int6
   }
 }
 
-__global__ void k_cic_gather_push(const double* __restrict__ g3, double* __restrict__ x,
+// Shared-memory deposit for small grids (N_g <= 32, the C5 coarse grid): the
+// grid's z range is cut into NZC chunks of ZC planes (N_g^2 ZC doubles <= 128 KB
+// of shared memory); blockIdx.y = chunk.  A CTA accumulates the weights of its
+// particles (grid-stride over blockIdx.x) that land in its chunk in shared
+// memory, then flushes the chunk with one REDG.ADD.F64 per non-zero node: 8
+// global atomics per particle become 8 shared ones plus N_g^2 ZC global ones
+// per CTA, and no two particles contend in L2.
+__global__ void __launch_bounds__(512) k_cic_deposit_smem(const double* __restrict__ x, int64_t stride,
+                                                          int64_t n, int Ng, int ZC, double inv_h,
+                                                          double* __restrict__ grid) {
+  extern __shared__ double tile[];
+  const int z0 = blockIdx.y * ZC;
+  const int nt = Ng * Ng * ZC;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) tile[i] = 0.0;
+  __syncthreads();
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int i0[3], i1[3];
+    double w0[3], w1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) cic_1d(x[d * stride + j], inv_h, Ng, i0[d], i1[d], w0[d], w1[d]);
+#pragma unroll
+    for (int cz = 0; cz < 2; ++cz) {
+      const int iz = (cz ? i1[2] : i0[2]) - z0;
+      if (iz < 0 || iz >= ZC) continue;
+      const double wz = cz ? w1[2] : w0[2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int ix = (c & 2) ? i1[0] : i0[0];
+        const int iy = (c & 1) ? i1[1] : i0[1];
+        const double wt = ((c & 2) ? w1[0] : w0[0]) * ((c & 1) ? w1[1] : w0[1]) * wz;
+        atomicAdd(&tile[(ix * Ng + iy) * ZC + iz], wt);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const double val = tile[i];
+    if (val != 0.0) {
+      const int iz = i % ZC, xy = i / ZC;
+      atomicAdd(grid + (int64_t)xy * Ng + z0 + iz, val);
+    }
+  }
+}
+
+// E on the nodes interleaved, {E_x, E_y, E_z, 0} per node (one 32-byte sector):
+// the gather's 8 nodes x 3 components become 8 sector reads instead of 24.
+__global__ void k_pic_interleave(const double* __restrict__ g3, int64_t npts, double4* __restrict__ gi) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npts;
+       j += (int64_t)gridDim.x * blockDim.x)
+    gi[j] = make_double4(g3[j], g3[npts + j], g3[2 * npts + j], 0.0);
+}
+
+__global__ void k_cic_gather_push(const double4* __restrict__ gi, double* __restrict__ x,
                                   double* __restrict__ v, int64_t stride, int64_t n, int Ng,
                                   double inv_h, PushArgs P) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
-  const int64_t n3 = (int64_t)Ng * Ng * Ng;
   double x0 = x[j], x1 = x[stride + j], x2 = x[2 * stride + j];
   int i0[3], i1[3];
   double w0[3], w1[3];
@@ -55,10 +107,12 @@ __global__ void k_cic_gather_push(const double* __restrict__ g3, double* __restr
     int iy = (c & 2) ? i1[1] : i0[1];
     int iz = (c & 1) ? i1[2] : i0[2];
     double wt = ((c & 4) ? w1[0] : w0[0]) * ((c & 2) ? w1[1] : w0[1]) * ((c & 1) ? w1[2] : w0[2]);
-    int64_t idx = ((int64_t)ix * Ng + iy) * Ng + iz;
-    E0 += wt * g3[idx];
-    E1 += wt * g3[n3 + idx];
-    E2 += wt * g3[2 * n3 + idx];
+    const double2* node = reinterpret_cast<const double2*>(gi + ((int64_t)ix * Ng + iy) * Ng + iz);
+    const double2 exy = __ldg(node);
+    const double ez = __ldg(reinterpret_cast<const double*>(node + 1));
+    E0 += wt * exy.x;
+    E1 += wt * exy.y;
+    E2 += wt * ez;
   }
   double v0 = v[j], v1 = v[stride + j], v2 = v[2 * stride + j];
   push_particle(x0, x1, x2, v0, v1, v2, E0, E1, E2, P);
@@ -172,13 +226,42 @@ cudaError_t launch_convert(double* d, float* f, int64_t count, bool to_float, cu
 
 cudaError_t launch_cic_deposit(const double* x, int64_t stride, int64_t n, int Ng, double inv_h,
                                double* grid, cudaStream_t st) {
-  if (n > 0) k_cic_deposit<<<nblk(n, 256), 256, 0, st>>>(x, stride, n, Ng, inv_h, grid);
+  if (n <= 0) return cudaSuccess;
+#ifndef PIF_CIC_SMEM
+#define PIF_CIC_SMEM 1
+#endif
+  if (PIF_CIC_SMEM && Ng <= 32) {
+    const int ZC = Ng < 16 ? Ng : 16, NZC = Ng / ZC;
+    const size_t smem = (size_t)Ng * Ng * ZC * sizeof(double);
+    static DevCache cache;
+    int ctas = 0;  // resident 512-thread CTAs on the device
+    cudaError_t e = dev_cached(cache, ctas, [&](int dev, int& val) {
+      int sms = 0, per = 0;
+      cudaError_t r = cudaFuncSetAttribute(k_cic_deposit_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(32 * 32 * 16 * sizeof(double)));
+      if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (r == cudaSuccess)
+        r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cic_deposit_smem, 512, 32 * 32 * 16 * sizeof(double));
+      val = sms * (per > 0 ? per : 1);
+      return r;
+    });
+    if (e != cudaSuccess) return e;
+    // enough particles per CTA that the chunk flush (Ng^2 ZC REDG) stays small
+    int64_t bx = std::min<int64_t>((n + 8191) / 8192, std::max(1, ctas / NZC));
+    k_cic_deposit_smem<<<dim3((unsigned)bx, NZC), 512, smem, st>>>(x, stride, n, Ng, ZC, inv_h, grid);
+    return cudaGetLastError();
+  }
+  k_cic_deposit<<<nblk(n, 256), 256, 0, st>>>(x, stride, n, Ng, inv_h, grid);
   return cudaGetLastError();
 }
-cudaError_t launch_cic_gather_push(const double* grid3, double* x, double* v, int64_t stride,
-                                   int64_t n, int Ng, double inv_h, const PushArgs& P,
+cudaError_t launch_cic_gather_push(const double* grid3, double* grid4, double* x, double* v,
+                                   int64_t stride, int64_t n, int Ng, double inv_h, const PushArgs& P,
                                    cudaStream_t st) {
-  if (n > 0) k_cic_gather_push<<<nblk(n, 256), 256, 0, st>>>(grid3, x, v, stride, n, Ng, inv_h, P);
+  const int64_t npts = (int64_t)Ng * Ng * Ng;
+  k_pic_interleave<<<nblk(npts, 256) < 1184 ? nblk(npts, 256) : 1184, 256, 0, st>>>(grid3, npts,
+                                                                                  (double4*)grid4);
+  if (n > 0)
+    k_cic_gather_push<<<nblk(n, 256), 256, 0, st>>>((const double4*)grid4, x, v, stride, n, Ng, inv_h, P);
   return cudaGetLastError();
 }
 cudaError_t launch_push_only(double* x, double* v, const double* E, int64_t stride, int64_t n,

@@ -208,6 +208,7 @@ struct Plan {
   double2* spec = nullptr;
   double2* G3 = nullptr;
   double* grid3 = nullptr;
+  double* grid4 = nullptr;  // PIC: interleaved field [n^3][4]
   double2* box = nullptr;
   double* cor = nullptr;  // 1/psi^(2 pi m / n), m in [-N/2, N/2]
   double* S = nullptr;    // S(k_m), m in [-N/2, N/2]
@@ -318,6 +319,7 @@ size_t layout(pif_ctx c, char* base) {
     take(p.grid3, 3 * p.grid_pts() * sizeof(double));
     if (p.fp32_ar)
       take(p.ar32, (p.kind == PIF_PROP_PIF_NUFFT ? 2 * p.box_elems() : p.grid_pts()) * sizeof(float));
+    if (p.kind == PIF_PROP_PIC_CIC) take(p.grid4, 4 * p.grid_pts() * sizeof(double));
     if (p.kind == PIF_PROP_PIF_NUFFT) {
       take(p.box, p.box_elems() * sizeof(double2));
       take(p.cor, (p.N + 1) * sizeof(double));
@@ -597,9 +599,9 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_FFT_INV, CUFFT(cufftExecZ2D(p.inv, (cufftDoubleComplex*)p.G3, p.grid3)));
     c->launches += 2;
     if (kicks > 0 || drift) {
-      PH(PH_PIC_GATHER_PUSH, CU(launch_cic_gather_push(p.grid3, c->xA, c->vA, n, n, Ng, 1.0 / h,
+      PH(PH_PIC_GATHER_PUSH, CU(launch_cic_gather_push(p.grid3, p.grid4, c->xA, c->vA, n, n, Ng, 1.0 / h,
                                                        P, c->st)));
-      c->launches += 1;
+      c->launches += 2;
     }
     c->box_fresh = (which == 0) && !drift;
   }

@@ -247,8 +247,9 @@ cudaError_t launch_cic_deposit(const double* x, int64_t stride, int64_t n, int N
                                double* grid, cudaStream_t st);
 cudaError_t launch_pic_poisson(const double2* spec, int Ng, double L, double scale, double2* G3,
                                cudaStream_t st);
-cudaError_t launch_cic_gather_push(const double* grid3, double* x, double* v, int64_t stride,
-                                   int64_t n, int Ng, double inv_h, const PushArgs& P,
+// grid4: [Ng^3][4] scratch for the interleaved field (one 32-byte sector per node)
+cudaError_t launch_cic_gather_push(const double* grid3, double* grid4, double* x, double* v,
+                                   int64_t stride, int64_t n, int Ng, double inv_h, const PushArgs& P,
                                    cudaStream_t st);
 cudaError_t launch_grid_energy(const double* grid3, int64_t npts, double h3, double* partials,
                                double* out4, cudaStream_t st);

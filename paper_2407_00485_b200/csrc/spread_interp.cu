@@ -1171,19 +1171,16 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
 #define PIF_SLAB(A, B, Cz, BX, BY, SBZ, CSX, ZR)                                                \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz && g.RS[0] == BX && g.RS[1] == BY &&       \
       g.ib[2] == SBZ && g.m[2] == 1 && (g.C == 1 || g.C == g.ib[0] * g.ib[1]))                 \
-    return interp_slab_launch<A, B, Cz, BX, BY, SBZ, CSX, ZR>(nsub, grid3, x, v, stride, id,     \
-                                                              Eout, offsets, g, hc, P, st);
+    return interp_slab_launch<A, B, Cz, BX, BY, SBZ, CSX, ZR>(nsub, grid3, x, v, stride, id, Eout,  \
+                                                              offsets, g, hc, P, st);
   PIF_SLAB(14, 14, 16, 16, 16, 4, 17, 0)  // w = 13: ring of 6 slabs without zero rows
   PIF_SLAB(10, 10, 8, 16, 16, 1, 17, 1)   // w = 8, dense
-  PIF_SLAB(6, 6, 8, 8, 8, 4, 9, 1)        // w = 5, dense
 #undef PIF_SLAB
 #endif
 #define PIF_INTERP(A, B, Cz)                                                                   \
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
   if (g.C != 1) return cudaErrorInvalidValue;  // cell keys need the slab kernel
-  PIF_INTERP(6, 6, 8)
-  PIF_INTERP(8, 8, 8)
   PIF_INTERP(10, 10, 8)
   PIF_INTERP(12, 12, 12)
   PIF_INTERP(14, 14, 16)
