@@ -48,7 +48,8 @@ CONFIGS = {1: ("landau", 32, 1 << 21, 1e-12, 0.05),     # C2
            7: ("landau", 64, 1 << 26, 1e-4, 0.05),        # C5 coarse (PIF, eps 1e-4) propagator (1 GPU)
            8: ("landau", 64, 1 << 26, 1e-4, 0.05),        # C5 coarse propagator in fp32 (PIF_FLAG_FP32)
            9: ("landau", 64, 1 << 22, 1e-4, 0.05),        # C5-reduced coarse propagator in fp32
-           10: ("landau", 32, 1 << 26, 0.0, 0.05)}        # C5 coarse G_B: CIC-PIC on a 32^3 grid
+           10: ("landau", 32, 1 << 26, 0.0, 0.05),        # C5 coarse G_B: CIC-PIC on a 32^3 grid
+           11: ("landau", 64, 1 << 24, 1e-7, 0.003125)}   # C5 fine share of one GPU out of 4 (space-only)
 FP32_CONFIGS = (8, 9)
 PIC_CONFIGS = (10,)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -218,7 +219,7 @@ def timed_steps(P, sim, stream, steps, flush, world, dist):
     return float(t.item()), phases, launches
 
 
-def c3_strong(args, P, rank, world, local, nccl_id, flush, dist):
+def c3_strong(args, P, rank, world, local, new_id, flush, dist):
     """BASELINE configs[2]: TSI, 32^3 modes, 2^23 particles in total split over
     the world (particle decomposition, rho_hat allreduce), tol 1e-12, dt 0.05."""
     import torch
@@ -230,7 +231,7 @@ def c3_strong(args, P, rank, world, local, nccl_id, flush, dist):
     p, x0, v0 = make_case(case, n_global, 2)  # the same global problem on every N
     sim = P.Simulation(P.physics(p.L, p.q_over_m, p.total_charge, p.B, p.A, p.c),
                        P.propagator("pif", N, dt, tol=tol), None, n_particles=n_global,
-                       device=local, rank=rank, world=world, space_size=world, nccl_id=nccl_id,
+                       device=local, rank=rank, world=world, space_size=world, nccl_id=new_id(),
                        stream=stream)
     a, c = sim.first, sim.n_local
     sim.set_state(torch.from_numpy(x0[:, a:a + c].copy()).to(dev), torch.from_numpy(v0[:, a:a + c].copy()).to(dev))
@@ -257,11 +258,15 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     if world > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=dev)
-    nccl_id = None
-    if world > 1:
+    def new_id():
+        """A fresh ncclUniqueId from rank 0 (one per communicator initialisation)."""
+        if world == 1:
+            return None
         obj = [P.pif_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
+
+    nccl_id = new_id()
     p, x0, v0 = make_case(CASE, N_PER_GPU, CFG + 1000 * rank)
     n_global = N_PER_GPU * world
     stream = torch.cuda.current_stream(dev)
@@ -349,7 +354,7 @@ def run_ours(args, rank, world, local):
 
     strong = None
     if CFG == 1 and not args.no_c3_strong:
-        strong = c3_strong(args, P, rank, world, local, nccl_id, flush, dist)
+        strong = c3_strong(args, P, rank, world, local, new_id, flush, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -370,7 +375,7 @@ def run_ours(args, rank, world, local):
                        "modes": N_MODES, "nufft_tol": TOL, "es_width": w, "es_beta": beta,
                        "upsampled_grid": n_up, "dt": DT, "l2": "flushed (256 MB write) between steps",
                        "parallelism": f"particle-decomposition x{world} (rho_hat allreduce)"},
-            "nccl": comm, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "nccl": dict(comm or {}, init_log=nccl_init_lines()), "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "phase_ms_per_step": {k: v / args.steps for k, v in phases.items() if v > 0},
             "c3_strong": strong,
@@ -378,6 +383,19 @@ def run_ours(args, rank, world, local):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def nccl_init_lines():
+    """NCCL INIT lines of this job's ranks (NCCL_DEBUG_FILE, see main)."""
+    import glob
+    pat = f"/tmp/pif_bench_nccl.{os.environ.get('MASTER_PORT', '0')}.*.log"
+    out = []
+    for f in sorted(glob.glob(pat)):
+        try:
+            out += [l.strip()[-160:] for l in open(f) if "Init COMPLETE" in l or "nRanks" in l or "nranks" in l]
+        except OSError:
+            pass
+    return out[:64]
 
 
 def spawn_ranks(args):
@@ -402,10 +420,11 @@ def main():
     if args.gpus > 1 and world == 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args))
     if world > 1:
-        # NCCL INIT logging (to stderr) shows every communicator's nranks
+        # NCCL INIT logging: every communicator's "Init COMPLETE ... nranks N"
+        # lines go to per-process files, which rank 0 quotes in the JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/pif_bench_nccl.{os.environ.get('MASTER_PORT', '0')}.%p.log")
     run_ours(args, rank, world, local)
 
 
