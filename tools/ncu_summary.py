@@ -24,7 +24,12 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
-        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio"]
 SHORT = {"k_interp_push": "interp_push", "k_spread": "spread", "k_bin_count": "bin_count",
          "k_scatter_sorted": "scatter_sorted", "k_scatter_index": "scatter_index",
          "k_gather_sorted": "gather_sorted"}
@@ -77,17 +82,18 @@ def main():
         lines.append(f"| `{k[:70]}` | {n} | {v:.0f} {unit} | {100 * v / tot:.1f} % |")
     open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
     rep = full(rpath)
+    nmain = len(rep)
     for e in extra:
         rep += full(e)
     lines = [f"# {tag}: `ncu --set full` key metrics", ""]
     traffic = {}
-    for name, m in rep:
-        lines.append(f"## `{name[:110]}`")
+    for i, (name, m) in enumerate(rep):
+        lines.append(f"## `{name[:110]}`" + ("" if i < nmain else " (extra report)"))
         for k, (v, u) in m.items():
             lines.append(f"- {k}: {v} {u or ''}")
         lines.append("")
         short = next((s for p, s in SHORT.items() if p in name), None)
-        if short and m["dram__bytes_read.sum"][0]:
+        if short and i < nmain and short not in traffic and m["dram__bytes_read.sum"][0]:
             b = to_bytes(m["dram__bytes_read.sum"][0], m["dram__bytes_read.sum"][1]) + \
                 to_bytes(m["dram__bytes_write.sum"][0], m["dram__bytes_write.sum"][1])
             traffic[short] = b
