@@ -352,10 +352,11 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
     // (RX RY) % 32 == 0).  w = 13 (eps = 1e-12): interpolation tiles 16x14x16
     // over 4x2x4-cell sub-bricks, spreading tiles 16^3 over 4^3-cell bricks.
     // Small tiles waste fewer FMAs on padding but carry fewer particles per CTA;
-    // below ~12 (w = 8) / ~8 (w = 5) particles per upsampled cell the per-CTA
+    // below ~4 (w = 8; 8 per cell: dense 2.14e9 vs 12^3 1.23e9 particles/s, 2 per
+    // cell: 12^3 better) / ~8 (w = 5) particles per upsampled cell the per-CTA
     // overheads win, so the larger tiles are kept there (measured).
 #ifndef PIF_W8_PPC
-#define PIF_W8_PPC 12.0
+#define PIF_W8_PPC 4.0
 #endif
 #ifndef PIF_W5_PPC
 #define PIF_W5_PPC 8.0
