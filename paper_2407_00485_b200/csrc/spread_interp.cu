@@ -716,10 +716,7 @@ struct SlabCfg {
 #ifndef PIF_SLAB_NW1
 #define PIF_SLAB_NW1 24  // one-row slabs (w = 8 dense: smaller psi rows, 80 registers)
 #endif
-#ifndef PIF_SLAB_NW2
-#define PIF_SLAB_NW2 24  // two-slab tiles (w = 5 dense)
-#endif
-  static constexpr int NWCAP = SBZ == 1 ? PIF_SLAB_NW1 : (NSZ == 2 ? PIF_SLAB_NW2 : PIF_SLAB_NW);
+  static constexpr int NWCAP = SBZ == 1 ? PIF_SLAB_NW1 : PIF_SLAB_NW;
   static constexpr int NW = NWFIT < NWCAP ? NWFIT : NWCAP;
   // psi rows are zero-filled to FILL entries (px < RX, py <= RY: the padded
   // columns of a window's last k step, pz < ZP)
@@ -1100,7 +1097,6 @@ cudaError_t launch_spread(const double* x, int64_t stride, const double* s, doub
     return spread_launch<A, B, Cz>(nbr, x, stride, s, s_uniform, offsets, g, hc, grid, st);
   PIF_SPREAD(8, 8, 8)
   PIF_SPREAD(12, 12, 12)
-  PIF_SPREAD(16, 16, 8)
   PIF_SPREAD(16, 16, 16)
 #undef PIF_SPREAD
   return cudaErrorInvalidValue;
@@ -1181,10 +1177,7 @@ cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_
   if (g.RI[0] == A && g.RI[1] == B && g.RI[2] == Cz)                                           \
     return interp_launch<A, B, Cz>(nsub, grid3, x, v, stride, id, Eout, offsets, g, hc, P, st);
   if (g.C != 1) return cudaErrorInvalidValue;  // cell keys need the slab kernel
-  PIF_INTERP(10, 10, 8)
   PIF_INTERP(12, 12, 12)
-  PIF_INTERP(14, 14, 16)
-  PIF_INTERP(16, 14, 16)
   PIF_INTERP(16, 16, 16)
 #undef PIF_INTERP
   return cudaErrorInvalidValue;

@@ -542,3 +542,18 @@ def test_fp32_flag_rejected_below_1e5():
     with pytest.raises(P.PifError) as e:
         sim_for(phys, P.propagator("pif", 8, 0.05, tol=1e-7, fp32=True), n=100)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("tol", [1e-7, 1e-10])
+def test_sparse_tiles_w8_w11(tol):
+    """Below 4 particles per upsampled cell, w = 8 keeps the 12^3 tile on the
+    per-item kernel; w = 11 (eps 1e-10) runs the 16^3 tile."""
+    phys = landau_physics()
+    npart = 3000
+    x, _ = landau_state(npart, 61)
+    rng = np.random.default_rng(62)
+    s = rng.standard_normal(npart)
+    c = rng.standard_normal((8, 8, 8)) + 1j * rng.standard_normal((8, 8, 8))
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=tol), n=npart)
+    assert rel_l2(P.pif_debug_type1(sim.ctx, 0, x, s, 8), O.nudft_type1(x, s, 8, phys.L)) <= 10 * tol
+    assert rel_l2(P.pif_debug_type2(sim.ctx, 0, c, x), O.nudft_type2(c, x, 8, phys.L)) <= 10 * tol
