@@ -375,7 +375,7 @@ def run_ours(args, rank, world, local):
                        "modes": N_MODES, "nufft_tol": TOL, "es_width": w, "es_beta": beta,
                        "upsampled_grid": n_up, "dt": DT, "l2": "flushed (256 MB write) between steps",
                        "parallelism": f"particle-decomposition x{world} (rho_hat allreduce)"},
-            "nccl": dict(comm or {}, init_log=nccl_init_lines()), "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "nccl": comm, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "phase_ms_per_step": {k: v / args.steps for k, v in phases.items() if v > 0},
             "c3_strong": strong,
@@ -383,19 +383,6 @@ def run_ours(args, rank, world, local):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def nccl_init_lines():
-    """NCCL INIT lines of this job's ranks (NCCL_DEBUG_FILE, see main)."""
-    import glob
-    pat = f"/tmp/pif_bench_nccl.{os.environ.get('MASTER_PORT', '0')}.*.log"
-    out = []
-    for f in sorted(glob.glob(pat)):
-        try:
-            out += [l.strip()[-160:] for l in open(f) if "Init COMPLETE" in l or "nRanks" in l or "nranks" in l]
-        except OSError:
-            pass
-    return out[:64]
 
 
 def spawn_ranks(args):
@@ -420,11 +407,12 @@ def main():
     if args.gpus > 1 and world == 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args))
     if world > 1:
-        # NCCL INIT logging: every communicator's "Init COMPLETE ... nranks N"
-        # lines go to per-process files, which rank 0 quotes in the JSON line
+        # NCCL INIT logging to stderr (every communicator's "... nranks N ...
+        # Init COMPLETE" line; stdout keeps the one JSON line); the JSON line
+        # carries the communicator sizes from ncclCommCount ("nccl")
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/pif_bench_nccl.{os.environ.get('MASTER_PORT', '0')}.%p.log")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     run_ours(args, rank, world, local)
 
 
