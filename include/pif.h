@@ -27,11 +27,12 @@
  * Ownership: every pointer passed in is BORROWED -- the library never frees it.
  * Device memory used by pif_step is one caller-allocated workspace
  * (pif_workspace_size / pif_set_workspace; the Python binding allocates it as
- * a torch uint8 tensor).  Two calls allocate temporaries outside it, stream-
- * ordered (cudaMallocAsync) and released before they return, on every exit
- * path: pif_parareal holds its parareal states there -- (2 n_slices + 4)
- * states of (6 n_local + 1) doubles with time_size == 1, 5 states per time
- * rank otherwise -- and the debug exports their input / sort buffers.  The
+ * a torch uint8 tensor).  Outside it: pif_parareal's states -- (2 n_slices +
+ * 4) states of (6 n_local + 1) doubles with time_size == 1, 5 states per time
+ * rank otherwise -- are allocated (cudaMalloc) by the first call, reused by
+ * later calls with the same n_local and freed by pif_finalize; the debug
+ * exports allocate their input / sort buffers stream-ordered (cudaMallocAsync)
+ * and release them before returning, on every exit path.  The
  * context handle is library-owned (pif_finalize releases it).  Every call runs
  * on the context's device (pif_dist.device) and restores the caller's current
  * device before returning.

@@ -237,6 +237,12 @@ struct pif_ctx_s {
   cudaStream_t st_comm = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_sent = nullptr;
   bool nccl_broken = false;  // communicators aborted (async error / timeout)
+  // parareal states (outside the workspace, include/pif.h): allocated by the
+  // first pif_parareal, reused by later calls of the same size, freed by
+  // pif_finalize -- a fresh multi-GB allocation per call costs seconds of page
+  // mapping inside the timed parareal window
+  std::vector<double*> pstates;
+  size_t pstate_doubles = 0;
   // workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -1028,8 +1034,20 @@ static pif_status parareal_window(pif_ctx c, double t0, double t1, int32_t n_sli
   // Parareal states live outside the workspace (include/pif.h): stream-ordered
   // allocations released on every exit path.
   DevBufs bufs(c->st);
+  if (c->pstate_doubles != (size_t)SZ) {
+    TRY(sync_stream(c, c->st));
+    for (double* q : c->pstates) cudaFree(q);
+    c->pstates.clear();
+    c->pstate_doubles = (size_t)SZ;
+  }
+  size_t next_state = 0;
   auto alloc = [&](double** p) -> pif_status {
-    CU(bufs.alloc(p, SZ * sizeof(double)));
+    if (next_state == c->pstates.size()) {
+      double* q = nullptr;
+      CU(cudaMalloc(&q, SZ * sizeof(double)));
+      c->pstates.push_back(q);
+    }
+    *p = c->pstates[next_state++];
     CU(cudaMemsetAsync(*p, 0, SZ * sizeof(double), c->st));
     return PIF_OK;
   };
@@ -1270,9 +1288,10 @@ pif_status pif_parareal(pif_ctx c, double t0, double t1, int32_t n_slices, int32
       // hand U_{n_slices} of this window from the last time rank to all time ranks
       double t0c = now();
       const int64_t n = c->nloc;
-      DevBufs hb(c->st);
-      double* buf = nullptr;
-      CU(hb.alloc(&buf, 6 * n * sizeof(double)));
+      // a parareal state buffer of the finished window (its final state is
+      // already in the context) carries the hand-off
+      double* buf = c->pstates.empty() ? nullptr : c->pstates[0];
+      if (!buf) return fail(PIF_ERR_STATE, "no parareal state buffer for the window hand-off");
       if (c->t_idx == c->time_size - 1) TRY(store_state(c, buf));
       NC(ncclBroadcast(buf, buf, 6 * n, ncclDouble, c->time_size - 1, c->comm_time, c->st));
       TRY(load_state(c, buf));
@@ -1353,6 +1372,7 @@ pif_status pif_finalize(pif_ctx c) {
   if (c->comm_time) ncclCommDestroy(c->comm_time);
   if (c->comm_world) ncclCommDestroy(c->comm_world);
   if (c->host_red) cudaFreeHost(c->host_red);
+  for (double* q : c->pstates) cudaFree(q);
   delete c;
   return PIF_OK;
 }
