@@ -15,6 +15,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pif_internal.cuh"
 
 using namespace pif;
@@ -527,11 +529,18 @@ pif_status ph_mark(pif_ctx c, int ph) {
   CU(cudaEventRecord(v[c->ev_used[ph]++], c->st));
   return PIF_OK;
 }
-#define PH(ph, body)            \
-  do {                          \
-    TRY(ph_mark(c, ph));        \
-    body;                       \
-    TRY(ph_mark(c, ph));        \
+// Each phase: CUDA events when profiling is on (pif_profile) and an NVTX range
+// (header-only NVTX v3: free unless a tool such as nsys / ncu attaches).
+const char* const kPhaseName[PH_COUNT] = {"pif.sort", "pif.spread", "pif.fft_fwd", "pif.box",
+                                          "pif.allreduce", "pif.poisson", "pif.fft_inv", "pif.interp_push",
+                                          "pif.pic_deposit", "pif.pic_gather_push", "pif.other"};
+#define PH(ph, body)                 \
+  do {                               \
+    nvtxRangePushA(kPhaseName[ph]);  \
+    TRY(ph_mark(c, ph));             \
+    body;                            \
+    TRY(ph_mark(c, ph));             \
+    nvtxRangePop();                  \
   } while (0)
 
 Sched sched_of(pif_ctx c, const Plan& p) {
