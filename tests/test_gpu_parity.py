@@ -557,3 +557,15 @@ def test_sparse_tiles_w8_w11(tol):
     sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=tol), n=npart)
     assert rel_l2(P.pif_debug_type1(sim.ctx, 0, x, s, 8), O.nudft_type1(x, s, 8, phys.L)) <= 10 * tol
     assert rel_l2(P.pif_debug_type2(sim.ctx, 0, c, x), O.nudft_type2(c, x, 8, phys.L)) <= 10 * tol
+
+
+def test_repeatability_of_atomic_spread():
+    """Reading c21: the spread flushes with fp64 atomics, so two runs
+    differ only in summation order -- 20 identical Landau steps agree to ~1e-13
+    relative (positions, velocities), not bitwise."""
+    phys = landau_physics()
+    x0, v0 = landau_state(16384, 71)
+    a = run_gpu(phys, P.propagator("pif", 8, 0.05, tol=1e-12), x0, v0, 20)
+    b = run_gpu(phys, P.propagator("pif", 8, 0.05, tol=1e-12), x0, v0, 20)
+    assert np.abs(O.min_image(a[0] - b[0], phys.L)).max() <= 1e-13 * phys.L
+    assert np.abs(a[1] - b[1]).max() <= 1e-13 * np.abs(a[1]).max()
