@@ -47,7 +47,7 @@ def test_type1_vs_nudft_C1(tol, signed):
     assert rel_l2(got, ref) <= 10 * tol
 
 
-@pytest.mark.parametrize("tol", [1e-12, 1e-7, 1e-4])
+@pytest.mark.parametrize("tol", [1e-12, 1e-7, 1e-4, 1e-3, 1e-2])  # w = 13, 8, 5, 4, 3
 def test_type2_vs_nudft_C1(tol):
     phys = landau_physics()
     x, _ = landau_state(16384, 0)
@@ -506,8 +506,8 @@ def test_set_state_wraps_positions_outside_the_box():
 
 
 # ------------------------------------------ f3: fp32 coarse propagator ------
-@pytest.mark.parametrize("tol", [1e-4, 1e-5])
-@pytest.mark.parametrize("npart", [16384, 16 * 16 ** 3 + 3])  # sparse 8^3 tile / dense 6x6x8 (w = 5)
+@pytest.mark.parametrize("tol", [1e-2, 1e-3, 1e-4, 1e-5])  # w = 3, 4, 5, 6
+@pytest.mark.parametrize("npart", [16384, 16 * 16 ** 3 + 3])  # sparse / dense tiles
 def test_fp32_type2_vs_nudft(tol, npart):
     """PIF_FLAG_FP32: the fp32 interpolation is within 10 eps of the
     exact NUDFT (fp32 rounding ~1e-7 relative << 10 eps for eps >= 1e-5)."""
