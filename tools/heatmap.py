@@ -43,7 +43,8 @@ def main():
     N, T, Ns = a.modes, 19.2, 16
     fine_tol, stop = (1e-4, 1e-5) if a.dtf >= 0.05 else (1e-7, 1e-8)
     coarse_tols = [1e-2, 1e-3] if a.dtf >= 0.05 else [1e-3, 1e-4, 1e-5]
-    ratios = [1, 2, 4, 8, 16] if a.dtf >= 0.05 else [4, 8, 16, 32]
+    # coarse steps must divide the slice length T / N_s = 1.2
+    ratios = [1, 2, 4, 8, 24] if a.dtf >= 0.05 else [4, 8, 16, 32]
     phys = landau_physics() if a.case == "landau" else penning_physics()
     n = a.pc * N ** 3
     x0, v0 = (landau_state if a.case == "landau" else penning_state)(n, 21)
@@ -54,7 +55,8 @@ def main():
     for coarse_kind in [("pif", e) for e in coarse_tols] + [("pic", None)]:
         for r in ratios:
             dtg = r * a.dtf
-            if (T / Ns) / dtg < 1 - 1e-9:
+            m = (T / Ns) / dtg
+            if m < 1 - 1e-9 or abs(m - round(m)) > 1e-9 * m:
                 continue
             coarse = (P.propagator("pif", N, dtg, tol=coarse_kind[1]) if coarse_kind[0] == "pif"
                       else P.propagator("pic", N, dtg))
