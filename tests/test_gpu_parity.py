@@ -167,12 +167,15 @@ def test_momentum_conservation_any_tolerance():
         assert np.abs(mom - mom0).max() <= 1e-13 * scale, (tol, mom - mom0)
 
 
-def test_pic_steps_vs_oracle():
-    """20 CIC-PIC steps (exact algorithm on both sides) <= 1e-12."""
+@pytest.mark.parametrize("Ng", [16, 32, 64])
+def test_pic_steps_vs_oracle(Ng):
+    """20 CIC-PIC steps (exact algorithm on both sides) <= 1e-12: one z-chunk of
+    the shared-memory deposit (16^3), two chunks (32^3, the C5 coarse grid) and
+    the global-atomic deposit (64^3)."""
     phys = landau_physics()
     x0, v0 = landau_state(8192, 7)
-    x, v, *_ = run_gpu(phys, P.propagator("pic", 16, 0.05), x0, v0, 20)
-    xr, vr = O.run(x0, v0, 20, O.Propagator("pic", 16, 0.05), O.PhysicsParams.from_inputs(phys))
+    x, v, *_ = run_gpu(phys, P.propagator("pic", Ng, 0.05), x0, v0, 20)
+    xr, vr = O.run(x0, v0, 20, O.Propagator("pic", Ng, 0.05), O.PhysicsParams.from_inputs(phys))
     assert np.abs(O.min_image(x - xr, phys.L)).max() <= 1e-12 * phys.L
     assert np.abs(v - vr).max() <= 1e-12 * np.abs(vr).max()
 
