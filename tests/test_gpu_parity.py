@@ -572,3 +572,10 @@ def test_repeatability_of_atomic_spread():
     b = run_gpu(phys, P.propagator("pif", 8, 0.05, tol=1e-12), x0, v0, 20)
     assert np.abs(O.min_image(a[0] - b[0], phys.L)).max() <= 1e-13 * phys.L
     assert np.abs(a[1] - b[1]).max() <= 1e-13 * np.abs(a[1]).max()
+
+
+def test_comm_info_single_process():
+    """pif_comm_info: communicator sizes are 1 without NCCL (world == 1)."""
+    phys = landau_physics()
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=1e-7), n=100)
+    assert sim.comm_info() == {"world_nranks": 1, "space_nranks": 1, "time_nranks": 1}
