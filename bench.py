@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3-strong", action="store_true")
+    ap.add_argument("--nccl-log", action="store_true", help="NCCL INIT logging (N > 1)")
     ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS),
                     help="BASELINE.json configs index (default 1 = the headline workload)")
     args = ap.parse_args()
@@ -406,13 +407,12 @@ def main():
         return
     if args.gpus > 1 and world == 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args))
-    if world > 1:
-        # NCCL INIT logging to stderr (every communicator's "... nranks N ...
-        # Init COMPLETE" line; stdout keeps the one JSON line); the JSON line
-        # carries the communicator sizes from ncclCommCount ("nccl")
+    if world > 1 and args.nccl_log:
+        # NCCL INIT logging (every communicator's "... nranks N ... Init
+        # COMPLETE" line, on NCCL's stdout); by default the JSON line's "nccl"
+        # key carries the communicator sizes from ncclCommCount instead
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     run_ours(args, rank, world, local)
 
 
