@@ -325,6 +325,17 @@ def run_ours(args, rank, world, local):
                     "frac": achieved / peak, "traffic": traffic, "kernel": dom,
                     "algorithmic": f"{flops_per_particle} FP64 flops/particle (w={w}: tensor product + ES kernel evaluation, SURVEY 8(d)) x {sim.n_local} particles per launch",
                     "peak_source": f"derived FP64: {SM_COUNT} SMs x {FP64_FMA_PER_SM_CLK} DFMA/clk x 2 x {sm_max:.0f} MHz"}
+        if dom == "interp_push" and w <= 5:
+            # the vector-pipe interpolation (w <= 5) is bound by shared-memory
+            # bandwidth: w^3 field nodes per particle, 24 B (fp64) / 12 B (fp32)
+            # each, against 128 B/clk/SM
+            bpn = 12 if CFG in FP32_CONFIGS else 24
+            smem_peak = SM_COUNT * 128 * sm_max * 1e6 / 1e12
+            got = sim.n_local * w ** 3 * bpn / launch_s / 1e12
+            roofline["smem"] = {"bound": "smem", "achieved": got, "peak": smem_peak, "unit": "TB/s",
+                                "frac": got / smem_peak,
+                                "algorithmic": f"{w ** 3} nodes x {bpn} B per particle (shared-memory loads)",
+                                "peak_source": f"{SM_COUNT} SMs x 128 B/clk x {sm_max:.0f} MHz"}
 
     # end-to-end through the public API with host (pinned) buffers
     e2e = None
