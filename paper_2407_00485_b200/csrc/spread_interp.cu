@@ -65,6 +65,15 @@ __device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bo
                : "memory");
 }
 
+// Bulk asynchronous reduction shared -> global (TMA, .add.f64), `cnt` doubles;
+// addresses 16-byte aligned, cnt even.  Completion: cp.async.bulk groups.
+__device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const double* ssrc, int cnt) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(gdst),
+               "r"(sa), "r"(cnt * 8)
+               : "memory");
+}
+
 // mbarrier (shared memory, CTA scope).
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -268,6 +277,11 @@ struct SpreadCfg {
   static constexpr int NW = NCT / CT;             // warps
   static constexpr int ZT = (RZ + 7) / 8;         // z tiles of 8 (psi_z rows zero-padded)
   static constexpr bool PADC = NCT * 8 != RX * RY;  // padded columns c >= RX RY (A = 0: py rows >= RY)
+  // TMA bulk-reduce flush: [column][z] tile rows of RZ doubles, 16-byte multiples
+#ifndef PIF_SPREAD_BULK
+#define PIF_SPREAD_BULK 1
+#endif
+  static constexpr bool BULK = PIF_SPREAD_BULK && (RZ % 2 == 0);
   // resident CTAs per SM the register budget must allow: small tiles (5 warps)
   // fit 5 by shared memory, and the register allocation decides between 3 and 4
   static constexpr int MINB = NW <= 5 ? 4 : PIF_SPREAD_MINB;
@@ -352,6 +366,40 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, SpreadCfg<RX, 
   }
   // flush: C[g][2t+i] = G[column (wid*CT+ct)*8 + gr][z = zt*8 + 2t + i]
   const int n = g.n;
+  if (C::BULK && (T0[2] & 1) == 0) {
+    // TMA bulk reduction (cp.reduce.async.bulk .add.f64, SASS UBLKRED): the tile
+    // goes to shared memory as [column][z] rows -- a column's z run is
+    // contiguous in the grid (z fastest) -- and each row is added to the grid
+    // by one bulk operation (two where it wraps the periodic z boundary)
+    // instead of RZ scalar REDG.ADD.F64.  Rows must be 16-byte aligned: RZ even
+    // (compile time) and an even tile origin T0z (n even keeps its parity).
+    // (The last chunk loop iteration ended with a barrier: psi is free.)
+    double* tile = &sm.px[0][0];
+#pragma unroll
+    for (int ct = 0; ct < C::CT; ++ct) {
+      const int col = acy[ct] * RX + acx[ct];
+#pragma unroll
+      for (int zt = 0; zt < C::ZT; ++zt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int z = zt * 8 + 2 * tq + i;
+          if (z < RZ && (!C::PADC || acy[ct] < RY)) tile[col * RZ + z] = acc[ct][zt][i] * s_uniform;
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async-proxy reads
+    __syncthreads();
+    const int gz0 = wrapi(T0[2], n);
+    const int seg = RZ < n - gz0 ? RZ : n - gz0;
+    for (int row = threadIdx.x; row < RX * RY; row += blockDim.x) {
+      const int cx = row % RX, cy = row / RX;
+      double* col = grid + ((int64_t)wrapi(T0[0] + cx, n) * n + wrapi(T0[1] + cy, n)) * n;
+      const double* src = tile + row * RZ;
+      bulk_reduce_add_f64(col + gz0, src, seg);
+      if (seg < RZ) bulk_reduce_add_f64(col, src + seg, RZ - seg);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem reads done before reuse
+  } else
 #pragma unroll
   for (int ct = 0; ct < C::CT; ++ct) {
     double* colp = grid + ((int64_t)wrapi(T0[0] + acx[ct], n) * n + wrapi(T0[1] + acy[ct], n)) * n;
