@@ -277,11 +277,14 @@ struct SpreadCfg {
   static constexpr int NW = NCT / CT;             // warps
   static constexpr int ZT = (RZ + 7) / 8;         // z tiles of 8 (psi_z rows zero-padded)
   static constexpr bool PADC = NCT * 8 != RX * RY;  // padded columns c >= RX RY (A = 0: py rows >= RY)
-  // TMA bulk-reduce flush: [column][z] tile rows of RZ doubles, 16-byte multiples
+  // TMA bulk-reduce flush: [column][z] tile rows of RZ doubles.  Used for the
+  // 16-deep brick tiles (128-byte rows; C2 spread 0.675 -> 0.668 ms, C4 5.31 ->
+  // 5.29 ms); the small sub-brick tiles (8-deep rows, many more items) measured
+  // slower with it (C5 coarse 4.44 -> 4.60, C5 fine 8.62 -> 8.86 ms)
 #ifndef PIF_SPREAD_BULK
 #define PIF_SPREAD_BULK 1
 #endif
-  static constexpr bool BULK = PIF_SPREAD_BULK && (RZ % 2 == 0);
+  static constexpr bool BULK = PIF_SPREAD_BULK && RZ >= 16 && RZ % 2 == 0;
   // resident CTAs per SM the register budget must allow: small tiles (5 warps)
   // fit 5 by shared memory, and the register allocation decides between 3 and 4
   static constexpr int MINB = NW <= 5 ? 4 : PIF_SPREAD_MINB;
