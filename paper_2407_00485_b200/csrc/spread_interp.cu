@@ -113,11 +113,34 @@ struct RowStride {
   static constexpr int v = R <= 8 ? 12 : (R <= 16 ? 20 : ((R + 11) / 16) * 16 + 4);
 };
 
+// Column tiles of 8 of a spreading tile: ceil(RX RY / 8), or more (padded) when
+// that gives more column tiles per warp (PIF_SPREAD_NCT13 for the 10x10 tile)
+#ifndef PIF_SPREAD_NCT13
+#define PIF_SPREAD_NCT13 13
+#endif
+__host__ __device__ constexpr int spread_nct(int RX, int RY) {
+  return (RX * RY + 7) / 8 == 13 ? PIF_SPREAD_NCT13 : (RX * RY + 7) / 8;
+}
+// py entries past RY that padded columns c >= RX RY read (A = 0 there)
+__host__ __device__ constexpr int spread_pad_rows(int RX, int RY) {
+  return (spread_nct(RX, RY) * 8 + RX - 1) / RX - RY;
+}
+
+// Spread staging, node-major: px[node][particle] (py with the rows the padded
+// columns read, pz zero-padded to a multiple of 8 nodes).  A staging warp's
+// lanes write consecutive particles of one node (conflict-free; the earlier
+// particle-major rows, stride 4 mod 16, put 4 lanes on every bank: 16 M / 356 M
+// store conflicts at C2 / C5 fine), and the row stride S = CH + 4 (4 mod 16)
+// keeps the A and B fragment reads (4 particles x 4 consecutive nodes per
+// half-warp) on distinct banks.
 template <int RX, int RY, int RZ, int CH = kChunk>
 struct Psi {
-  double px[CH][RowStride<RX>::v];
-  double py[CH][RowStride<RY>::v];
-  double pz[CH][RowStride<(RZ + 7) / 8 * 8>::v];  // z rows zero-padded to a multiple of 8
+  static constexpr int S = CH + 4;
+  static constexpr int PY = RY + spread_pad_rows(RX, RY);
+  static constexpr int ZP = (RZ + 7) / 8 * 8;
+  double px[RX][S];
+  double py[PY][S];
+  double pz[ZP][S];
   double xs[CH][3];
   int rel[CH][3];
   double str[CH];
@@ -166,7 +189,7 @@ __device__ __forceinline__ void stage_position(Psi<RX, RY, RZ, CH>& sm, int tid,
 // ~15 FMAs per pair instead of 14 steps and 30 FMAs); the centre node of an odd
 // w is even in s (E only).  All pairs are evaluated in one pass: the FP64 pipe
 // is shared with the DMMAs, so dependent steps, not FMAs, set the latency.
-template <int NPAIR, bool CENTER>
+template <int NPAIR, bool CENTER, int ST = 1>
 __device__ __forceinline__ void horner_sym(double* row, int rel, double f, double sv,
                                            const Horner& hc, const Brick& g, double two_over_w) {
   constexpr int w = 2 * NPAIR + 2 + (CENTER ? 1 : 0);
@@ -179,8 +202,8 @@ __device__ __forceinline__ void horner_sym(double* row, int rel, double f, doubl
   constexpr int P0 = w <= 4 ? 1 : 0;
 #endif
   if (P0) {
-    row[rel] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
-    row[rel + w - 1] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
+    row[rel * ST] = es_kernel((double)(-g.hw) - f, two_over_w, g.beta);
+    row[(rel + w - 1) * ST] = es_kernel((double)(w - 1 - g.hw) - f, two_over_w, g.beta);
   }
   constexpr int NP = NPAIR + 1 - P0;         // polynomial pairs: nodes (P0 + i, w - 1 - P0 - i)
   constexpr int NE = NP + (CENTER ? 1 : 0);  // even parts (+ the centre node of an odd w)
@@ -200,35 +223,24 @@ __device__ __forceinline__ void horner_sym(double* row, int rel, double f, doubl
   }
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
-    row[rel + P0 + i] = fma(sv, o[i], e[i]);
-    row[rel + w - 1 - P0 - i] = fma(-sv, o[i], e[i]);
+    row[(rel + P0 + i) * ST] = fma(sv, o[i], e[i]);
+    row[(rel + w - 1 - P0 - i) * ST] = fma(-sv, o[i], e[i]);
   }
-  if (CENTER) row[rel + P0 + NP] = e[NP];
+  if (CENTER) row[(rel + P0 + NP) * ST] = e[NP];
 }
 
+// The w weights at row[(rel + k) ST], k < w (ST: element stride of the row).
+template <int ST = 1>
 __device__ __forceinline__ void psi_row(double* row, int rel, double f, double sv,
                                         const Horner& hc, const Brick& g, double two_over_w) {
   switch (g.w) {  // uniform
 #define PIF_W(W) \
-  case W: horner_sym<(W - 2) / 2, (W & 1) == 1>(row, rel, f, sv, hc, g, two_over_w); break;
+  case W: horner_sym<(W - 2) / 2, (W & 1) == 1, ST>(row, rel, f, sv, hc, g, two_over_w); break;
     PIF_W(2) PIF_W(3) PIF_W(4) PIF_W(5) PIF_W(6) PIF_W(7) PIF_W(8) PIF_W(9)
     PIF_W(10) PIF_W(11) PIF_W(12) PIF_W(13) PIF_W(14) PIF_W(15) PIF_W(16)
 #undef PIF_W
     default: break;
   }
-}
-
-// Column tiles of 8 of a spreading tile: ceil(RX RY / 8), or more (padded) when
-// that gives more column tiles per warp (PIF_SPREAD_NCT13 for the 10x10 tile)
-#ifndef PIF_SPREAD_NCT13
-#define PIF_SPREAD_NCT13 13
-#endif
-__host__ __device__ constexpr int spread_nct(int RX, int RY) {
-  return (RX * RY + 7) / 8 == 13 ? PIF_SPREAD_NCT13 : (RX * RY + 7) / 8;
-}
-// py entries past RY that padded columns c >= RX RY read (A = 0 there)
-__host__ __device__ constexpr int spread_pad_rows(int RX, int RY) {
-  return (spread_nct(RX, RY) * 8 + RX - 1) / RX - RY;
 }
 
 // ES weights of the chunk's particles (positions already staged); particles
@@ -242,26 +254,25 @@ __device__ __forceinline__ void stage_psi(Psi<RX, RY, RZ, CH>& sm, int cnt, int 
   const double two_over_w = 2.0 / g.w;
   const double flo = g.odd ? -0.5 : 0.0;
   const int w = g.w;
-  // item = (dimension, particle): a warp's lanes share the dimension.  (A
-  // cooperative zero fill of all rows with 16-byte stores measured slower:
-  // C2 spread 0.673 -> 0.739 ms, C5 fine 8.6 -> 10.7 ms.)
+  using PS = Psi<RX, RY, RZ, CH>;
+  constexpr int S = PS::S;
+  // item = (dimension, particle): a warp's lanes share the dimension and write
+  // consecutive particles of each node (node-major rows, see Psi)
   for (int it = threadIdx.x; it < 3 * pad; it += blockDim.x) {
     const int d = it / pad, p = it - d * pad;
-    const int R = d == 0 ? RX : (d == 1 ? RY : (RZ + 7) / 8 * 8);
-    double* row = d == 0 ? sm.px[p] : (d == 1 ? sm.py[p] : sm.pz[p]);
+    const int R = d == 0 ? RX : (d == 1 ? PS::PY : PS::ZP);
+    double* col = d == 0 ? &sm.px[0][p] : (d == 1 ? &sm.py[0][p] : &sm.pz[0][p]);
     if (p >= cnt) {
-      for (int u = 0; u < R + (d == 1 ? spread_pad_rows(RX, RY) : 0); ++u) row[u] = 0.0;
+      for (int u = 0; u < R; ++u) col[u * S] = 0.0;
       continue;
     }
     const int rel = sm.rel[p][d];
     const int T0d = d == 0 ? T0[0] : (d == 1 ? T0[1] : T0[2]);
     const double f = sm.xs[p][d] - (double)(rel + g.hw + T0d);  // x~ - anchor
-    for (int u = 0; u < rel; ++u) row[u] = 0.0;
-    for (int u = rel + w; u < R; ++u) row[u] = 0.0;
-    if (d == 1)  // padded spread columns read py[RY ..]
-      for (int u = R; u < R + spread_pad_rows(RX, RY); ++u) row[u] = 0.0;
+    for (int u = 0; u < rel; ++u) col[u * S] = 0.0;
+    for (int u = rel + w; u < R; ++u) col[u * S] = 0.0;  // (py: through the padded-column rows)
     const double sv = 2.0 * (f - flo) - 1.0;
-    psi_row(row, rel, f, sv, hc, g, two_over_w);
+    psi_row<S>(col, rel, f, sv, hc, g, two_over_w);
   }
   __syncthreads();
 }
@@ -288,7 +299,8 @@ struct SpreadCfg {
   // resident CTAs per SM the register budget must allow: small tiles (5 warps)
   // fit 5 by shared memory, and the register allocation decides between 3 and 4
   static constexpr int MINB = NW <= 5 ? 4 : PIF_SPREAD_MINB;
-  static_assert(RY + spread_pad_rows(RX, RY) <= RowStride<RY>::v, "py row stride");
+  static_assert((RX + RY + spread_pad_rows(RX, RY) + (RZ + 7) / 8 * 8) * (kChunk + 4) >= RX * RY * RZ,
+                "the bulk-flush tile reuses the psi rows");
   static_assert(NCT % CT == 0, "tile shape");
 };
 
@@ -354,12 +366,12 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, SpreadCfg<RX, 
       const int pl = p0 + tq;  // K index of this lane's A and B elements
       double b[C::ZT];
 #pragma unroll
-      for (int zt = 0; zt < C::ZT; ++zt) b[zt] = sm.pz[pl][zt * 8 + gr];
+      for (int zt = 0; zt < C::ZT; ++zt) b[zt] = sm.pz[zt * 8 + gr][pl];
       double sp = 1.0;
       if (HAS_S) sp = pl < cnt ? sm.str[pl] : 0.0;
 #pragma unroll
       for (int ct = 0; ct < C::CT; ++ct) {
-        double a = sm.px[pl][acx[ct]] * sm.py[pl][acy[ct]];
+        double a = sm.px[acx[ct]][pl] * sm.py[acy[ct]][pl];
         if (HAS_S) a *= sp;
 #pragma unroll
         for (int zt = 0; zt < C::ZT; ++zt) dmma(acc[ct][zt], a, b[zt]);
