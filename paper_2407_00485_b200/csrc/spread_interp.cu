@@ -436,6 +436,202 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, SpreadCfg<RX, 
   }
 }
 
+// ------------------------------------------------- spread, warp-owned items --
+// The sub-brick tiles (10x10x8 at w = 8, 6x6x8 at w = 5) with one WARP per
+// interpolation item instead of one CTA: the warp stages the psi rows of 32
+// particles at a time (lane = particle, all three dimensions) into its own
+// shared-memory rows and runs the k loop over ALL column tiles of the tile, so
+// there is no CTA barrier, and the A operand of a column tile,
+// W[c][p] = psi_x[cx][p] psi_y[cy][p], reuses one factor across tiles: the
+// columns of a tile are chosen so that, per lane, one of cx / cy is the same in
+// every tile of a group (WTile), loaded once per k step.  Shared-memory loads
+// per DMMA: 17 / 13 (10x10) and 7 / 5 (6x6) instead of 3 (two A factors + B) --
+// the CTA kernel above is shared-memory bound at these tiles (ncu, C5 fine: LSU
+// 85 %).  Accumulators stay in registers for the whole item (flush: one
+// REDG.ADD.F64 per tile node, as above).
+template <int RX, int RY>
+struct WTile;
+template <>
+struct WTile<10, 10> {
+  // tiles 0-9: row cy = ct, cx = gr (px[gr] shared); 10, 11: column cx = 8, 9,
+  // cy = gr (py[gr] shared); 12: the 2 x 2 corner (cx, cy >= 8) on rows 0-3
+  static constexpr int NCT = 13;
+  __host__ __device__ static constexpr int group(int ct) { return ct < 10 ? 0 : (ct < 12 ? 1 : 2); }
+  __device__ static bool col(int ct, int gr, int& cx, int& cy) {
+    if (ct < 10) { cx = gr; cy = ct; return true; }
+    if (ct < 12) { cx = 8 + ct - 10; cy = gr; return true; }
+    cx = 8 + (gr & 1);
+    cy = 8 + ((gr >> 1) & 1);
+    return gr < 4;
+  }
+};
+template <>
+struct WTile<6, 6> {
+  // tiles 0-4: rows 0-5 of the fragment cx = gr, cy = ct (px[gr] shared); rows
+  // 6, 7 take the last row cy = 5, cx = 2 ct + gr - 6 (py[5] shared), tiles 0-2
+  static constexpr int NCT = 5;
+  __host__ __device__ static constexpr int group(int) { return 0; }
+  __device__ static bool col(int ct, int gr, int& cx, int& cy) {
+    if (gr < 6) { cx = gr; cy = ct; return true; }
+    cx = 2 * ct + gr - 6;
+    cy = 5;
+    return ct <= 2;
+  }
+};
+
+template <int RX, int RY, int RZ>
+struct SpreadWCfg {
+  using TP = WTile<RX, RY>;
+  static constexpr int NCT = TP::NCT;
+  static constexpr int ZT = (RZ + 7) / 8;
+  static constexpr int MP = 32;                 // particles per staging round (lane = particle)
+  static constexpr int S = MP + 4;              // node-major row stride (4 mod 16)
+  static constexpr int ZR = RX + RY;            // the zero row (padded columns)
+  static constexpr int OZ = RX + RY + 1;        // first psi_z row
+  static constexpr int ROWS = OZ + ZT * 8;
+  static constexpr int NW = 4;                  // warps per CTA (each on its own items)
+  static constexpr int MINB = NCT > 8 ? 5 : 7;  // resident CTAs per SM (registers, no spills)
+};
+
+template <int RX, int RY, int RZ, bool HAS_S>
+__global__ void __launch_bounds__(32 * SpreadWCfg<RX, RY, RZ>::NW, SpreadWCfg<RX, RY, RZ>::MINB)
+    k_spread_warp(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
+                  double s_uniform, const Sched Sc, Brick g,
+                  const __grid_constant__ Horner hc, double* __restrict__ grid) {
+  using C = SpreadWCfg<RX, RY, RZ>;
+  using TP = typename C::TP;
+  constexpr int S = C::S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* const Q = reinterpret_cast<double*>(smem_raw) + wid * (C::ROWS * S);
+  const int gr = lane >> 2, tq = lane & 3;
+  const int n = g.n, w = g.w;
+  const double two_over_w = 2.0 / w;
+  const double flo = g.odd ? -0.5 : 0.0;
+  // zero row (never written again)
+  if (lane < S) Q[C::ZR * S + lane] = 0.0;
+  if (lane + 32 < S) Q[C::ZR * S + lane + 32] = 0.0;
+  // per-lane A rows: tile ct reads T[ct] (node-major row offset) and, in groups
+  // 0 / 1, the shared factor H0 / H1; group 2 reads both factors per tile
+  int toff[C::NCT], goff[C::NCT];
+  int h0 = C::ZR * S, h1 = C::ZR * S;
+#pragma unroll
+  for (int ct = 0; ct < C::NCT; ++ct) {
+    // shared factor of this lane in the tile's group: the coordinate that is
+    // the same in the group's first two tiles (a one-tile group: px)
+    int first = -1, second = -1;
+#pragma unroll
+    for (int u = 0; u < C::NCT; ++u)
+      if (TP::group(u) == TP::group(ct)) {
+        if (first < 0) first = u;
+        else if (second < 0) second = u;
+      }
+    int cx, cy, fx, fy, sx = 0, sy = 0;
+    const bool ok = TP::col(ct, gr, cx, cy);
+    TP::col(first, gr, fx, fy);
+    if (second >= 0) TP::col(second, gr, sx, sy);
+    const bool share_x = second < 0 || fx == sx;
+    const int hrow = share_x ? cx : RX + cy;
+    const int trow = share_x ? RX + cy : cx;
+    toff[ct] = ok ? trow * S : C::ZR * S;
+    goff[ct] = TP::group(ct) == 2 ? hrow * S : 0;
+    if (TP::group(ct) == 0 && ct == first) h0 = hrow * S;
+    if (TP::group(ct) == 1 && ct == first) h1 = hrow * S;
+  }
+  const int total = Sc.ioff[Sc.nkeys];
+  int item = blockIdx.x * C::NW + wid;
+  while (item < total) {
+    int claimed = 0;
+    if (lane == 0) claimed = gridDim.x * C::NW + atomicAdd(Sc.ctr, 1);
+    const int4 e = Sc.iitems[item];
+    const int4 f = Sc.iinfo[item];  // {bx, by, bz, sx | sy << 16}
+    const int64_t start = e.y, end = e.z;
+    int T0[3];
+    T0[0] = f.x * g.sb[0] - g.hw + (f.w & 0xffff) * g.ib[0];
+    T0[1] = f.y * g.sb[1] - g.hw + (f.w >> 16) * g.ib[1];
+    T0[2] = f.z * g.sb[2] - g.hw;
+    double acc[C::NCT][C::ZT][2];
+#pragma unroll
+    for (int ct = 0; ct < C::NCT; ++ct)
+#pragma unroll
+      for (int zt = 0; zt < C::ZT; ++zt) acc[ct][zt][0] = acc[ct][zt][1] = 0.0;
+    double xr[3] = {0.0, 0.0, 0.0}, sr = 0.0;
+    if (start + lane < end) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) xr[d] = x[d * stride + start + lane];
+      if (HAS_S) sr = s[start + lane];
+    }
+    for (int64_t base = start; base < end; base += C::MP) {
+      const int cnt = (int)min((int64_t)C::MP, end - base);
+      __syncwarp();  // the previous round's k loop is done with Q
+      // lane = particle: the psi rows of all three dimensions (zeros outside the
+      // window and for lanes past cnt)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int R = d == 0 ? RX : (d == 1 ? RY : C::ZT * 8);
+        double* col = Q + (d == 0 ? 0 : (d == 1 ? RX : C::OZ)) * S + lane;
+        int rel = R;
+        double fr = 0.0;
+        if (lane < cnt) {
+          double xs = xr[d] * g.scale;
+          const int a = anchor_of(xs, g);
+          rel = a - g.hw - T0[d];
+          fr = xs - (double)a;
+        }
+        for (int u = 0; u < R; ++u)
+          if (u < rel || u >= rel + w) col[u * S] = 0.0;
+        if (lane < cnt) {
+          const double sv = 2.0 * (fr - flo) - 1.0;
+          psi_row<S>(col, rel, fr, sv, hc, g, two_over_w);
+          if (HAS_S && d == 2)
+            for (int u = 0; u < w; ++u) col[(rel + u) * S] *= sr;
+        }
+      }
+      // prefetch the next round's positions (consumed after this k loop)
+      if (base + C::MP + lane < end) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) xr[d] = x[d * stride + base + C::MP + lane];
+        if (HAS_S) sr = s[base + C::MP + lane];
+      }
+      __syncwarp();
+      const int pad = (cnt + 3) & ~3;
+#pragma unroll 2
+      for (int p0 = 0; p0 < pad; p0 += 4) {
+        const int pl = p0 + tq;
+        double b[C::ZT];
+#pragma unroll
+        for (int zt = 0; zt < C::ZT; ++zt) b[zt] = Q[(C::OZ + zt * 8 + gr) * S + pl];
+        const double H0 = Q[h0 + pl];
+        const double H1 = Q[h1 + pl];
+#pragma unroll
+        for (int ct = 0; ct < C::NCT; ++ct) {
+          const double t = Q[toff[ct] + pl];
+          const double hv = TP::group(ct) == 0 ? H0 : (TP::group(ct) == 1 ? H1 : Q[goff[ct] + pl]);
+          const double a = hv * t;
+#pragma unroll
+          for (int zt = 0; zt < C::ZT; ++zt) dmma(acc[ct][zt], a, b[zt]);
+        }
+      }
+    }
+    // flush: C[gr][2 tq + i] = G[column TP::col(ct, gr)][z = 8 zt + 2 tq + i]
+#pragma unroll
+    for (int ct = 0; ct < C::NCT; ++ct) {
+      int cx, cy;
+      if (!TP::col(ct, gr, cx, cy)) continue;
+      double* colp = grid + ((int64_t)wrapi(T0[0] + cx, n) * n + wrapi(T0[1] + cy, n)) * n;
+#pragma unroll
+      for (int zt = 0; zt < C::ZT; ++zt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double val = acc[ct][zt][i];
+          const int z = zt * 8 + 2 * tq + i;
+          if (z < RZ && val != 0.0) atomicAdd(colp + wrapi(T0[2] + z, n), val * s_uniform);
+        }
+    }
+    item = __shfl_sync(0xffffffffu, claimed, 0);
+  }
+}
+
 // ------------------------------------------------------------ interp+push --
 // "K = columns" formulation: every warp owns whole m-tiles of 8 particles and
 // contracts over all tile columns,
@@ -1150,9 +1346,53 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
   return cudaGetLastError();
 }
 
+#ifndef PIF_SPREAD_WARP
+#define PIF_SPREAD_WARP 1
+#endif
+template <int A, int B, int Cz>
+static cudaError_t spread_warp_launch(unsigned nitems, const double* x, int64_t stride, const double* s,
+                                      double s_uniform, const Sched& offsets, const Brick& g,
+                                      const Horner& hc, double* grid, cudaStream_t st) {
+  using C = SpreadWCfg<A, B, Cz>;
+  const int T = 32 * C::NW;
+  const size_t smem = sizeof(double) * C::NW * C::ROWS * C::S;
+  static DevCache cache;
+  int ctas = 0;  // resident CTAs on the device
+  cudaError_t e = dev_cached(cache, ctas, [&](int dev, int& v) {
+    int sms = 0, per = 0;
+    cudaError_t r = cudaFuncSetAttribute(k_spread_warp<A, B, Cz, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(k_spread_warp<A, B, Cz, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (r == cudaSuccess)
+      r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_spread_warp<A, B, Cz, false>, T, smem);
+    v = sms * per;
+    return r;
+  });
+  if (e != cudaSuccess) return e;
+  unsigned nbr = (nitems + C::NW - 1) / C::NW;
+  if ((int64_t)nbr > (int64_t)ctas) nbr = ctas;  // persistent: one wave, items claimed by warps
+  if (nbr == 0) return cudaSuccess;
+  cudaError_t e0 = cudaMemsetAsync(offsets.ctr, 0, sizeof(int), st);
+  if (e0 != cudaSuccess) return e0;
+  if (s)
+    k_spread_warp<A, B, Cz, true><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+  else
+    k_spread_warp<A, B, Cz, false><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
                           const Sched& offsets, const Brick& g, const Horner& hc, double* grid,
                           cudaStream_t st) {
+  if (PIF_SPREAD_WARP && g.C > 1 && g.RI[0] == 10 && g.RI[1] == 10 && g.RI[2] == 8)
+    return spread_warp_launch<10, 10, 8>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
+                                         g, hc, grid, st);
+  if (PIF_SPREAD_WARP && g.C > 1 && g.RI[0] == 6 && g.RI[1] == 6 && g.RI[2] == 8)
+    return spread_warp_launch<6, 6, 8>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
+                                       g, hc, grid, st);
   // dense w = 8 / w = 5 plans (>= 12 / 8 particles per cell, cell keys): spread
   // over the interpolation sub-bricks with the interpolation tile (10x10x8 /
   // 6x6x8 instead of 16x16x8 / 8^3: 2.6x / 1.8x fewer padded FMAs), the extra
