@@ -390,6 +390,8 @@ pif_status make_plan(pif_ctx c, int which, const pif_propagator* pr) {
       g.sb[d] = g.ib[d] * m[d];
       g.RS[d] = g.sb[d] + w - 1;
       g.NB[d] = (n + g.sb[d] - 1) / g.sb[d];
+      g.rsb[d] = 1.0f / (float)g.sb[d];
+      g.rib[d] = 1.0f / (float)g.ib[d];
       g.nkeys *= (int64_t)g.NB[d] * m[d];
     }
     // slab interpolation tiles: keys down to the xy-cells of a sub-brick, so an

@@ -46,6 +46,8 @@ struct Brick {
   int64_t nkeys; // number of sub-bricks = NB0 NB1 NB2 m0 m1 m2
   double scale;  // n / L (grid units per length)
   double beta;   // ES shape parameter
+  float rsb[3];  // 1 / sb, 1 / ib (binning: floor(a / d) = (int)((a + 1/2) / d) in fp32,
+  float rib[3];  //  exact for a < 2^16, d <= 64: the quotient is >= 1/(2d) from an integer)
 };
 
 // Piecewise-polynomial ES kernel: for a particle

@@ -15,9 +15,10 @@ __global__ void k_bin_count(const double* __restrict__ x, int64_t stride, int64_
   for (int d = 0; d < 3; ++d) {
     double xs = x[d * stride + j] * g.scale;
     int a = anchor_of(xs, g);
-    B[d] = a / g.sb[d];
+    // a / sb, r / ib without the integer-division sequences (Brick::rsb)
+    B[d] = (int)(((float)a + 0.5f) * g.rsb[d]);
     const int r = a - B[d] * g.sb[d];
-    S[d] = r / g.ib[d];
+    S[d] = (int)(((float)r + 0.5f) * g.rib[d]);
     Q[d] = r - S[d] * g.ib[d];
   }
   int k = ((B[0] * g.NB[1] + B[1]) * g.NB[2] + B[2]) * (g.m[0] * g.m[1] * g.m[2]) +
