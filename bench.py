@@ -315,8 +315,8 @@ def run_ours(args, rank, world, local):
         flops_per_particle = {"spread": 2 * w ** 3, "interp_push": 6 * w ** 3}[dom] + 6 * w * (w + 3)
         achieved = sim.n_local * flops_per_particle / launch_s / 1e12
         peak = SM_COUNT * FP64_FMA_PER_SM_CLK * 2 * sm_max * 1e6 / 1e12
-        traffic = None
-        if os.path.exists(TRAFFIC_FILE):
+        traffic = None  # the committed ncu capture is of the default (C2) step only
+        if CFG == 1 and os.path.exists(TRAFFIC_FILE):
             try:
                 traffic = json.load(open(TRAFFIC_FILE)).get(dom)
             except Exception:
