@@ -91,11 +91,13 @@ typedef struct {
                            halves the communication, the "single precision for the density
                            field" of P:553-554 (meant for coarse propagators).
                            bit 1 PIF_FLAG_FP32: single-precision coarse propagator (P:553-554,
-                           "future work"): the type-2 interpolation (grid tile, kernel weights,
-                           accumulation) runs in fp32 on the vector pipe; positions, velocities,
-                           the push, the spread and the FFTs stay fp64.  PIF kind only, tol >=
-                           1e-5 (w <= 6; fp32 rounding ~1e-7 stays far inside 10 eps), else
-                           PIF_ERR_ARG.  0 = default. */
+                           "future work"): the inverse FFT (C2R) and the type-2 interpolation
+                           (grid tile, kernel weights, accumulation) run in fp32 on the vector
+                           pipe; the spread accumulates in fp64 (DMMA) with its kernel weights
+                           evaluated in fp32 on the dense tiles; positions, velocities, the
+                           push, the forward FFT and the Poisson solve stay fp64.  PIF kind
+                           only, tol >= 1e-5 (w <= 6; fp32 rounding ~1e-7 stays far inside
+                           10 eps), else PIF_ERR_ARG.  0 = default. */
   double tol;           /* PIF: NUFFT tolerance eps in [1e-15, 1e-1); ignored for PIC */
   double dt;            /* timestep > 0 */
 } pif_propagator;

@@ -21,38 +21,6 @@
 
 namespace pif {
 
-// psi[k] = psi_ES(k - hw - f) for the w window nodes, from the per-node
-// polynomials in s (spread_interp.cu:horner_sym, here into registers): node
-// w-1-k at s is node k at -s, so each pair costs one even/odd Horner split.
-template <typename T, int W, typename HC>
-__device__ __forceinline__ void psi_regs(T (&p)[W], T s, double f, const HC& hc, const Brick& g) {
-  constexpr int NPAIR = W / 2;
-  constexpr int P0 = W <= 4 ? 1 : 0;  // edge nodes exact for w <= 4 (fit error 0.25 eps)
-  const T s2 = s * s;
-#pragma unroll
-  for (int i = P0; i < NPAIR; ++i) {
-    T e = (T)hc.a[i][kHornerDeg], o = (T)hc.a[i][kHornerDeg - 1];
-#pragma unroll
-    for (int j = kHornerDeg / 2 - 1; j >= 0; --j) {
-      e = fma(e, s2, (T)hc.a[i][2 * j]);
-      if (j < kHornerDeg / 2 - 1) o = fma(o, s2, (T)hc.a[i][2 * j + 1]);
-    }
-    p[i] = fma(s, o, e);
-    p[W - 1 - i] = fma(-s, o, e);
-  }
-  if (W & 1) {
-    T e = (T)hc.a[W / 2][kHornerDeg];
-#pragma unroll
-    for (int j = kHornerDeg / 2 - 1; j >= 0; --j) e = fma(e, s2, (T)hc.a[W / 2][2 * j]);
-    p[W / 2] = e;
-  }
-  if (P0) {
-    const double tw = 2.0 / W;
-    p[0] = (T)es_kernel((double)(-g.hw) - f, tw, g.beta);
-    p[W - 1] = (T)es_kernel((double)(W - 1 - g.hw) - f, tw, g.beta);
-  }
-}
-
 template <typename T>
 __device__ __forceinline__ void cp_async_t(T* smem, const T* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);

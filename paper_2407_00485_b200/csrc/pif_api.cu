@@ -588,7 +588,8 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
     PH(PH_SORT, TRY(sort_particles(c, p)));
     PH(PH_SPREAD, {
       CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-      CU(launch_spread(c->xA, n, nullptr, 1.0, sched_of(c, p), p.g, p.hc, p.grid, c->st));
+      CU(launch_spread(c->xA, n, nullptr, 1.0, sched_of(c, p), p.g, p.hc, p.fp32 ? &p.hcf : nullptr,
+                        p.grid, c->st));
     });
     PH(PH_FFT_FWD, CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec)));
     const double L = c->ph.L;
@@ -1452,7 +1453,7 @@ pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, con
   double2* dout = nullptr;
   CU(B.alloc(&dout, N3 * sizeof(double2)));
   CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-  CU(launch_spread(D.x2, n, D.s2, 1.0, D.S, p.g, p.hc, p.grid, c->st));
+  CU(launch_spread(D.x2, n, D.s2, 1.0, D.S, p.g, p.hc, p.fp32 ? &p.hcf : nullptr, p.grid, c->st));
   CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec));
   CU(launch_debug_extract_KN(p.spec, p.n, p.N, p.cor, dout, c->st));
   CU(cudaMemcpyAsync(out, dout, N3 * sizeof(double2), cudaMemcpyDeviceToHost, c->st));

@@ -89,6 +89,39 @@ __device__ __forceinline__ double es_kernel(double t, double two_over_w, double 
   return r > 0.0 ? exp(beta * (sqrt(r) - 1.0)) : (r == 0.0 ? exp(-beta) : 0.0);
 }
 
+// psi[k] = psi_ES(k - hw - f) for the w window nodes, from the per-node
+// polynomials in s (spread_interp.cu:horner_sym, here into registers; used by interp_simt.cu and
+// the fp32 staging of spread_interp.cu:k_spread_warp): node
+// w-1-k at s is node k at -s, so each pair costs one even/odd Horner split.
+template <typename T, int W, typename HC>
+__device__ __forceinline__ void psi_regs(T (&p)[W], T s, double f, const HC& hc, const Brick& g) {
+  constexpr int NPAIR = W / 2;
+  constexpr int P0 = W <= 4 ? 1 : 0;  // edge nodes exact for w <= 4 (fit error 0.25 eps)
+  const T s2 = s * s;
+#pragma unroll
+  for (int i = P0; i < NPAIR; ++i) {
+    T e = (T)hc.a[i][kHornerDeg], o = (T)hc.a[i][kHornerDeg - 1];
+#pragma unroll
+    for (int j = kHornerDeg / 2 - 1; j >= 0; --j) {
+      e = fma(e, s2, (T)hc.a[i][2 * j]);
+      if (j < kHornerDeg / 2 - 1) o = fma(o, s2, (T)hc.a[i][2 * j + 1]);
+    }
+    p[i] = fma(s, o, e);
+    p[W - 1 - i] = fma(-s, o, e);
+  }
+  if (W & 1) {
+    T e = (T)hc.a[W / 2][kHornerDeg];
+#pragma unroll
+    for (int j = kHornerDeg / 2 - 1; j >= 0; --j) e = fma(e, s2, (T)hc.a[W / 2][2 * j]);
+    p[W / 2] = e;
+  }
+  if (P0) {
+    const double tw = 2.0 / W;
+    p[0] = (T)es_kernel((double)(-g.hw) - f, tw, g.beta);
+    p[W - 1] = (T)es_kernel((double)(W - 1 - g.hw) - f, tw, g.beta);
+  }
+}
+
 // x - L floor(x / L), L itself mapped to 0.  For 0 <= x < L, x / L rounds to at
 // most 1 - 2^-53 (x <= L - ulp(L)), so floor(x / L) = 0 and the result is x:
 // the division (a ~10-instruction FP64 sequence) runs only for crossing particles.
@@ -218,9 +251,11 @@ cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id
                                  int64_t stride, int64_t n, const int* key, const int* rank,
                                  const int* offsets, int* perm, double* x2, double* v2, int* id2,
                                  double* s2, cudaStream_t st);
+// hcf != null (fp32 plans): the warp-owned dense-tile spread evaluates the ES
+// weights from the fp32 coefficients in single precision (stored as fp64)
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const Sched& S, const Brick& g, const Horner& hc, double* grid,
-                          cudaStream_t st);
+                          const Sched& S, const Brick& g, const Horner& hc, const HornerF* hcf,
+                          double* grid, cudaStream_t st);
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
                                const int* id, double* Eout, const Sched& S, const Brick& g,
                                const Horner& hc, const PushArgs& P, cudaStream_t st);

@@ -25,6 +25,8 @@
 //
 // Fragment layouts of m8n8k4.f64 (lane l, g = l >> 2, t = l & 3):
 //   A (8x4, row): A[g][t];  B (4x8, col): B[t][g];  C (8x8): C[g][2t], C[g][2t+1].
+#include <type_traits>
+
 #include "pif_internal.cuh"
 
 namespace pif {
@@ -479,6 +481,25 @@ struct WTile<6, 6> {
   }
 };
 
+// The w weights in fp32 (fp32 plans, eps >= 1e-5: the weights' ~1e-7 relative
+// error is far below eps) at row[(rel + k) ST]: the Horner chains run on the
+// FP32 pipe instead of the FP64 datapath the DMMAs use.
+template <int ST>
+__device__ __forceinline__ void psi_row_f32(double* row, int rel, double f, double sv,
+                                            const HornerF& hc, const Brick& g) {
+  switch (g.w) {  // uniform
+#define PIF_W(W)                                                          \
+  case W: {                                                               \
+    float pv[W];                                                          \
+    psi_regs<float, W>(pv, (float)sv, f, hc, g);                          \
+    _Pragma("unroll") for (int k = 0; k < W; ++k) row[(rel + k) * ST] = pv[k]; \
+  } break;
+    PIF_W(2) PIF_W(3) PIF_W(4) PIF_W(5) PIF_W(6) PIF_W(7) PIF_W(8)
+#undef PIF_W
+    default: break;
+  }
+}
+
 template <int RX, int RY, int RZ>
 struct SpreadWCfg {
   using TP = WTile<RX, RY>;
@@ -493,11 +514,11 @@ struct SpreadWCfg {
   static constexpr int MINB = NCT > 8 ? 5 : 7;  // resident CTAs per SM (registers, no spills)
 };
 
-template <int RX, int RY, int RZ, bool HAS_S>
+template <int RX, int RY, int RZ, bool HAS_S, typename HC>
 __global__ void __launch_bounds__(32 * SpreadWCfg<RX, RY, RZ>::NW, SpreadWCfg<RX, RY, RZ>::MINB)
     k_spread_warp(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
                   double s_uniform, const Sched Sc, Brick g,
-                  const __grid_constant__ Horner hc, double* __restrict__ grid) {
+                  const __grid_constant__ HC hc, double* __restrict__ grid) {
   using C = SpreadWCfg<RX, RY, RZ>;
   using TP = typename C::TP;
   constexpr int S = C::S;
@@ -582,7 +603,8 @@ __global__ void __launch_bounds__(32 * SpreadWCfg<RX, RY, RZ>::NW, SpreadWCfg<RX
           if (u < rel || u >= rel + w) col[u * S] = 0.0;
         if (lane < cnt) {
           const double sv = 2.0 * (fr - flo) - 1.0;
-          psi_row<S>(col, rel, fr, sv, hc, g, two_over_w);
+          if constexpr (std::is_same<HC, HornerF>::value) psi_row_f32<S>(col, rel, fr, sv, hc, g);
+          else psi_row<S>(col, rel, fr, sv, hc, g, two_over_w);
           if (HAS_S && d == 2)
             for (int u = 0; u < w; ++u) col[(rel + u) * S] *= sr;
         }
@@ -1349,10 +1371,10 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
 #ifndef PIF_SPREAD_WARP
 #define PIF_SPREAD_WARP 1
 #endif
-template <int A, int B, int Cz>
+template <int A, int B, int Cz, typename HC>
 static cudaError_t spread_warp_launch(unsigned nitems, const double* x, int64_t stride, const double* s,
                                       double s_uniform, const Sched& offsets, const Brick& g,
-                                      const Horner& hc, double* grid, cudaStream_t st) {
+                                      const HC& hc, double* grid, cudaStream_t st) {
   using C = SpreadWCfg<A, B, Cz>;
   const int T = 32 * C::NW;
   const size_t smem = sizeof(double) * C::NW * C::ROWS * C::S;
@@ -1360,14 +1382,14 @@ static cudaError_t spread_warp_launch(unsigned nitems, const double* x, int64_t 
   int ctas = 0;  // resident CTAs on the device
   cudaError_t e = dev_cached(cache, ctas, [&](int dev, int& v) {
     int sms = 0, per = 0;
-    cudaError_t r = cudaFuncSetAttribute(k_spread_warp<A, B, Cz, true>,
+    cudaError_t r = cudaFuncSetAttribute(k_spread_warp<A, B, Cz, true, HC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(k_spread_warp<A, B, Cz, false>,
+      r = cudaFuncSetAttribute(k_spread_warp<A, B, Cz, false, HC>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (r == cudaSuccess)
-      r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_spread_warp<A, B, Cz, false>, T, smem);
+      r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_spread_warp<A, B, Cz, false, HC>, T, smem);
     v = sms * per;
     return r;
   });
@@ -1378,21 +1400,27 @@ static cudaError_t spread_warp_launch(unsigned nitems, const double* x, int64_t 
   cudaError_t e0 = cudaMemsetAsync(offsets.ctr, 0, sizeof(int), st);
   if (e0 != cudaSuccess) return e0;
   if (s)
-    k_spread_warp<A, B, Cz, true><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread_warp<A, B, Cz, true, HC><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
   else
-    k_spread_warp<A, B, Cz, false><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread_warp<A, B, Cz, false, HC><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
   return cudaGetLastError();
 }
 
+#ifndef PIF_SPREAD_F32PSI
+#define PIF_SPREAD_F32PSI 1
+#endif
 cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const Sched& offsets, const Brick& g, const Horner& hc, double* grid,
-                          cudaStream_t st) {
+                          const Sched& offsets, const Brick& g, const Horner& hc, const HornerF* hcf,
+                          double* grid, cudaStream_t st) {
+  const unsigned ni = (unsigned)offsets.max_i;
   if (PIF_SPREAD_WARP && g.C > 1 && g.RI[0] == 10 && g.RI[1] == 10 && g.RI[2] == 8)
-    return spread_warp_launch<10, 10, 8>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
-                                         g, hc, grid, st);
+    return (PIF_SPREAD_F32PSI && hcf)
+               ? spread_warp_launch<10, 10, 8>(ni, x, stride, s, s_uniform, offsets, g, *hcf, grid, st)
+               : spread_warp_launch<10, 10, 8>(ni, x, stride, s, s_uniform, offsets, g, hc, grid, st);
   if (PIF_SPREAD_WARP && g.C > 1 && g.RI[0] == 6 && g.RI[1] == 6 && g.RI[2] == 8)
-    return spread_warp_launch<6, 6, 8>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
-                                       g, hc, grid, st);
+    return (PIF_SPREAD_F32PSI && hcf)
+               ? spread_warp_launch<6, 6, 8>(ni, x, stride, s, s_uniform, offsets, g, *hcf, grid, st)
+               : spread_warp_launch<6, 6, 8>(ni, x, stride, s, s_uniform, offsets, g, hc, grid, st);
   // dense w = 8 / w = 5 plans (>= 12 / 8 particles per cell, cell keys): spread
   // over the interpolation sub-bricks with the interpolation tile (10x10x8 /
   // 6x6x8 instead of 16x16x8 / 8^3: 2.6x / 1.8x fewer padded FMAs), the extra
