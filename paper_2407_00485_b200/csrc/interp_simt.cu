@@ -103,12 +103,18 @@ __global__ void __launch_bounds__(128) k_interp_push_simt(const T* __restrict__ 
     const T* tz = gz[buf];
     int j = start + threadIdx.x;
     double xr[3] = {0.0, 0.0, 0.0};
-    if (j < end) xr[0] = x[j], xr[1] = x[stride + j], xr[2] = x[2 * stride + j];
+    if (j < end) {
+      const int64_t sj = src_of(P.perm, j);
+      xr[0] = x[sj], xr[1] = x[stride + sj], xr[2] = x[2 * stride + sj];
+    }
     for (; j < end; j += blockDim.x) {
       // positions of this thread's next particle in flight during this one
       const int jn = j + blockDim.x;
       double xn[3] = {0.0, 0.0, 0.0};
-      if (jn < end) xn[0] = x[jn], xn[1] = x[stride + jn], xn[2] = x[2 * stride + jn];
+      if (jn < end) {
+        const int64_t sn = src_of(P.perm, jn);
+        xn[0] = x[sn], xn[1] = x[stride + sn], xn[2] = x[2 * stride + sn];
+      }
       int rel[3];
       T px[W], py[W], pz[W];
 #pragma unroll
@@ -144,21 +150,25 @@ __global__ void __launch_bounds__(128) k_interp_push_simt(const T* __restrict__ 
           E2 = fma(wxy, t2, E2);
         }
       }
+      const int64_t sj = src_of(P.perm, j);
       if (Eout) {
-        const int64_t k = id[j];
+        const int64_t k = id[sj];
         Eout[k] = (double)E0;
         Eout[stride + k] = (double)E1;
         Eout[2 * stride + k] = (double)E2;
       }
       if (P.kicks > 0 || P.drift) {
-        double v0 = v[j], v1 = v[stride + j], v2 = v[2 * stride + j];
+        double v0 = v[sj], v1 = v[stride + sj], v2 = v[2 * stride + sj];
         push_particle(xr[0], xr[1], xr[2], v0, v1, v2, (double)E0, (double)E1, (double)E2, P);
-        x[j] = xr[0];
-        x[stride + j] = xr[1];
-        x[2 * stride + j] = xr[2];
-        v[j] = v0;
-        v[stride + j] = v1;
-        v[2 * stride + j] = v2;
+        double* const xo = P.xo ? P.xo : x;
+        double* const vo = P.vo ? P.vo : v;
+        xo[j] = xr[0];
+        xo[stride + j] = xr[1];
+        xo[2 * stride + j] = xr[2];
+        vo[j] = v0;
+        vo[stride + j] = v1;
+        vo[2 * stride + j] = v2;
+        if (P.ido) P.ido[j] = id[sj];
       }
       xr[0] = xn[0];
       xr[1] = xn[1];

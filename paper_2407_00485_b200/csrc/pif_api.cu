@@ -552,11 +552,23 @@ Sched sched_of(pif_ctx c, const Plan& p) {
 }
 
 // a0: counting sort of the working particles (xA, vA, idA) by brick of plan p.
-pif_status sort_particles(pif_ctx c, Plan& p) {
+// fused (PIF_FUSED_SORT): only the permutation perm[sorted j] = current index is
+// built; the spread reads x through it and the interpolation + push reads x, v,
+// id through it and writes the pushed particles in sorted order into xB, vB,
+// idB (then swapped in) -- the separate gather pass (~108 B per particle of HBM
+// traffic) disappears.  Otherwise the particles are gathered here.
+#ifndef PIF_FUSED_SORT
+#define PIF_FUSED_SORT 1
+#endif
+pif_status sort_particles(pif_ctx c, Plan& p, bool fused) {
   const int64_t n = c->nloc;
   CU(cudaMemsetAsync(c->counts, 0, p.nbricks * sizeof(int), c->st));
   CU(launch_bin_count(c->xA, n, n, p.g, c->key, c->rnk, c->counts, c->st));
   CU(launch_schedule(c->counts, sched_of(c, p), p.g, keys_per_brick(p.g), p.g.C, c->st));
+  if (fused) {
+    CU(launch_scatter_index(n, c->key, c->rnk, c->offsets, c->perm, c->st));
+    return PIF_OK;
+  }
   CU(launch_gather_sorted(c->xA, c->vA, c->idA, nullptr, n, n, c->key, c->rnk, c->offsets, c->perm,
                           c->xB, c->vB, c->idB, nullptr, c->st));
   std::swap(c->xA, c->xB);
@@ -585,11 +597,16 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
   const int64_t n = c->nloc;
   PushArgs P = push_args(c, p, kicks, drift);
   if (p.kind == PIF_PROP_PIF_NUFFT) {
-    PH(PH_SORT, TRY(sort_particles(c, p)));
+    // a push (kicks or drift) writes the sorted copy; a field-only solve (the
+    // diagnostics' box) leaves the particles where they are
+    const bool push = kicks > 0 || drift;
+    const bool fused = PIF_FUSED_SORT && push;
+    const int* perm = fused ? c->perm : nullptr;
+    PH(PH_SORT, TRY(sort_particles(c, p, fused)));
     PH(PH_SPREAD, {
       CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-      CU(launch_spread(c->xA, n, nullptr, 1.0, sched_of(c, p), p.g, p.hc, p.fp32 ? &p.hcf : nullptr,
-                        p.grid, c->st));
+      CU(launch_spread(c->xA, perm, n, nullptr, 1.0, sched_of(c, p), p.g, p.hc,
+                        p.fp32 ? &p.hcf : nullptr, p.grid, c->st));
     });
     PH(PH_FFT_FWD, CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec)));
     const double L = c->ph.L;
@@ -598,10 +615,21 @@ pif_status solve_and_push(pif_ctx c, int which, int kicks, int drift) {
       PH(PH_ALLREDUCE, TRY(density_allreduce(c, p, (double*)p.box, 2 * p.box_elems())));
     PH(PH_POISSON, CU(launch_poisson_pad(p.box, p.n, p.N, L, p.cor, p.S, p.G3, p.fp32, c->st)));
     PH(PH_FFT_INV, CUFFT(inverse_fft(p)));
-    PH(PH_INTERP_PUSH, CU(interp_push(c, p, c->xA, c->vA, n, c->idA, nullptr, sched_of(c, p), P)));
+    if (fused) {
+      P.perm = c->perm;
+      P.xo = c->xB;
+      P.vo = c->vB;
+      P.ido = c->idB;
+    }
+    if (push) PH(PH_INTERP_PUSH, CU(interp_push(c, p, c->xA, c->vA, n, c->idA, nullptr, sched_of(c, p), P)));
+    if (fused) {
+      std::swap(c->xA, c->xB);
+      std::swap(c->vA, c->vB);
+      std::swap(c->idA, c->idB);
+    }
     // own kernels: bin, schedule (reduce, partials, apply, fill), sort (index
-    // scatter + gather), spread, extract, poisson, interp_push (cuFFT not counted)
-    c->launches += 11;
+    // scatter [+ gather]), spread, extract, poisson, interp_push (cuFFT not counted)
+    c->launches += 9 + (fused ? 0 : 1) + (push ? 1 : 0);
     c->box_fresh = (which == 0) && !drift;
   } else {
     const int Ng = p.n;
@@ -1453,7 +1481,7 @@ pif_status pif_debug_type1(pif_ctx c, int which, const double* x, int64_t n, con
   double2* dout = nullptr;
   CU(B.alloc(&dout, N3 * sizeof(double2)));
   CU(cudaMemsetAsync(p.grid, 0, p.grid_pts() * sizeof(double), c->st));
-  CU(launch_spread(D.x2, n, D.s2, 1.0, D.S, p.g, p.hc, p.fp32 ? &p.hcf : nullptr, p.grid, c->st));
+  CU(launch_spread(D.x2, nullptr, n, D.s2, 1.0, D.S, p.g, p.hc, p.fp32 ? &p.hcf : nullptr, p.grid, c->st));
   CUFFT(cufftExecD2Z(p.fwd, p.grid, (cufftDoubleComplex*)p.spec));
   CU(launch_debug_extract_KN(p.spec, p.n, p.N, p.cor, dout, c->st));
   CU(cudaMemcpyAsync(out, dout, N3 * sizeof(double2), cudaMemcpyDeviceToHost, c->st));

@@ -157,7 +157,17 @@ struct PushArgs {
   int magnetic, has_ext;
   int kicks;                // 0, 1 or 2 half kicks
   int drift;                // 1: x <- wrap(x + dt v)
+  // Sort fused into the push (pif_api.cu:sort_particles): perm != null -- the
+  // particle at sorted position j is x[perm[j]] (the input arrays stay in the
+  // previous order), and the pushed x, v and its id go to xo, vo, ido at j (the
+  // other buffers).  perm == null: in place at j.
+  const int* perm;
+  double* xo;
+  double* vo;
+  int* ido;
 };
+// Source index of sorted position j.
+__device__ __forceinline__ int64_t src_of(const int* perm, int64_t j) { return perm ? (int64_t)perm[j] : j; }
 
 __device__ __forceinline__ void push_particle(double& x0, double& x1, double& x2, double& v0,
                                               double& v1, double& v2, double E0, double E1,
@@ -251,11 +261,15 @@ cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id
                                  int64_t stride, int64_t n, const int* key, const int* rank,
                                  const int* offsets, int* perm, double* x2, double* v2, int* id2,
                                  double* s2, cudaStream_t st);
+// perm[offsets[key] + rank] = j only (the fused sort: spread and interp+push read
+// through perm, the push writes the sorted copy, PushArgs::perm)
+cudaError_t launch_scatter_index(int64_t n, const int* key, const int* rank, const int* offsets,
+                                 int* perm, cudaStream_t st);
 // hcf != null (fp32 plans): the warp-owned dense-tile spread evaluates the ES
 // weights from the fp32 coefficients in single precision (stored as fp64)
-cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const Sched& S, const Brick& g, const Horner& hc, const HornerF* hcf,
-                          double* grid, cudaStream_t st);
+cudaError_t launch_spread(const double* x, const int* perm, int64_t stride, const double* s,
+                          double s_uniform, const Sched& S, const Brick& g, const Horner& hc,
+                          const HornerF* hcf, double* grid, cudaStream_t st);
 cudaError_t launch_interp_push(const double* grid3, double* x, double* v, int64_t stride,
                                const int* id, double* Eout, const Sched& S, const Brick& g,
                                const Horner& hc, const PushArgs& P, cudaStream_t st);

@@ -304,6 +304,11 @@ cudaError_t launch_gather_sorted(const double* x, const double* v, const int* id
   }
   return cudaGetLastError();
 }
+cudaError_t launch_scatter_index(int64_t n, const int* key, const int* rank, const int* offsets,
+                                 int* perm, cudaStream_t st) {
+  if (n > 0) k_scatter_index<<<nblk(n, 256), 256, 0, st>>>(n, key, rank, offsets, perm);
+  return cudaGetLastError();
+}
 cudaError_t launch_iota(int* id, int64_t n, cudaStream_t st) {
   if (n > 0) k_iota<<<nblk(n, 256), 256, 0, st>>>(id, n);
   return cudaGetLastError();

@@ -311,7 +311,8 @@ struct SpreadCfg {
 // REDG.ADD.F64 per particle in the flush.
 template <int RX, int RY, int RZ, bool HAS_S, bool SUB>
 __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, SpreadCfg<RX, RY, RZ>::MINB)
-    k_spread(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
+    k_spread(const double* __restrict__ x, const int* __restrict__ perm, int64_t stride,
+             const double* __restrict__ s,
              double s_uniform, const Sched Sc, Brick g,
              const __grid_constant__ Horner hc, double* __restrict__ grid) {
   using C = SpreadCfg<RX, RY, RZ>;
@@ -359,7 +360,8 @@ __global__ void __launch_bounds__(32 * SpreadCfg<RX, RY, RZ>::NW, SpreadCfg<RX, 
     const int cnt = (int)min((int64_t)kChunk, end - base);
     const int pad = (cnt + 3) & ~3;
     for (int q = tid; q < cnt; q += blockDim.x) {
-      double xr[3] = {x[base + q], x[stride + base + q], x[2 * stride + base + q]};
+      const int64_t sq = src_of(perm, base + q);
+      double xr[3] = {x[sq], x[stride + sq], x[2 * stride + sq]};
       stage_position(sm, q, xr, g, T0);
       if (HAS_S) sm.str[q] = s[base + q];
     }
@@ -516,7 +518,8 @@ struct SpreadWCfg {
 
 template <int RX, int RY, int RZ, bool HAS_S, typename HC>
 __global__ void __launch_bounds__(32 * SpreadWCfg<RX, RY, RZ>::NW, SpreadWCfg<RX, RY, RZ>::MINB)
-    k_spread_warp(const double* __restrict__ x, int64_t stride, const double* __restrict__ s,
+    k_spread_warp(const double* __restrict__ x, const int* __restrict__ perm, int64_t stride,
+                  const double* __restrict__ s,
                   double s_uniform, const Sched Sc, Brick g,
                   const __grid_constant__ HC hc, double* __restrict__ grid) {
   using C = SpreadWCfg<RX, RY, RZ>;
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(32 * SpreadWCfg<RX, RY, RZ>::NW, SpreadWCfg<RX
     double xr[3] = {0.0, 0.0, 0.0}, sr = 0.0;
     if (start + lane < end) {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) xr[d] = x[d * stride + start + lane];
+      for (int d = 0; d < 3; ++d) xr[d] = x[d * stride + src_of(perm, start + lane)];
       if (HAS_S) sr = s[start + lane];
     }
     for (int64_t base = start; base < end; base += C::MP) {
@@ -612,7 +615,7 @@ __global__ void __launch_bounds__(32 * SpreadWCfg<RX, RY, RZ>::NW, SpreadWCfg<RX
       // prefetch the next round's positions (consumed after this k loop)
       if (base + C::MP + lane < end) {
 #pragma unroll
-        for (int d = 0; d < 3; ++d) xr[d] = x[d * stride + base + C::MP + lane];
+        for (int d = 0; d < 3; ++d) xr[d] = x[d * stride + src_of(perm, base + C::MP + lane)];
         if (HAS_S) sr = s[base + C::MP + lane];
       }
       __syncwarp();
@@ -822,6 +825,7 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
   c.base = pf.base = 0;
   cursor_load(c, g, Sc);
   pf = c;
+  auto pp = c;  // perm prefetch cursor (fused sort)
   auto advance = [&](ItemCursor& it, int q, bool release) {
     while (it.k < nitems && q >= it.base + it.m) {
       if (release) {
@@ -835,15 +839,27 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
     return it.k < nitems;
   };
   // x, v of m-tile q -> xv[buf] (one cp.async group, possibly empty)
-  auto prefetch = [&](int buf, int q) {
+  // fused sort: the source index of this lane's particle (p = lane & 7) of an
+  // m-tile, loaded one prefetch ahead (cursor pp) so that its latency does not
+  // stall the cp.async issue
+  auto perm_of = [&](int q) -> int {
+    int r = 0;
+    if (P.perm && advance(pp, q, false)) {
+      const int64_t b = pp.start + 8 * (int64_t)(q - pp.base) + (lane & 7);
+      if (b < pp.end) r = P.perm[b];
+    }
+    return r;
+  };
+  auto prefetch = [&](int buf, int q, int ps) {
     if (advance(pf, q, false)) {
       const int64_t b = pf.start + 8 * (int64_t)(q - pf.base);
       const int cnt = (int)min((int64_t)8, pf.end - b);
       for (int u = lane; u < 48; u += 32) {
         const int comp = u >> 3, p = u & 7;
         if (p < cnt) {
-          if (comp < 3) cp_async8(&xv[buf][comp][p], x + comp * stride + b + p);
-          else if (v) cp_async8(&xv[buf][comp][p], v + (comp - 3) * stride + b + p);
+          const int64_t sj = P.perm ? (int64_t)ps : b + p;
+          if (comp < 3) cp_async8(&xv[buf][comp][p], x + comp * stride + sj);
+          else if (v) cp_async8(&xv[buf][comp][p], v + (comp - 3) * stride + sj);
         }
       }
     }
@@ -874,11 +890,13 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
   };
 
   int buf = 0;
-  prefetch(0, wid);
+  prefetch(0, wid, perm_of(wid));
+  int pn = perm_of(wid + C::NW);
   for (int q = wid; advance(c, q, true); q += C::NW, buf ^= 1) {
     const int64_t b = c.start + 8 * (int64_t)(q - c.base);
     const int cnt = (int)min((int64_t)8, c.end - b);
-    prefetch(buf ^ 1, q + C::NW);  // xv[buf ^ 1] was released by the previous m-tile
+    prefetch(buf ^ 1, q + C::NW, pn);  // xv[buf ^ 1] was released by the previous m-tile
+    pn = perm_of(q + 2 * C::NW);
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
     stage(buf, cnt);
@@ -924,9 +942,9 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
       e2 += __shfl_xor_sync(0xffffffffu, e2, o);
     }
     if (tq == 0 && gr < cnt) {
-      const int64_t j = b + gr;
+      const int64_t j = b + gr, sj = src_of(P.perm, j);
       if (Eout) {
-        const int64_t k = id[j];
+        const int64_t k = id[sj];
         Eout[k] = e0;
         Eout[stride + k] = e1;
         Eout[2 * stride + k] = e2;
@@ -935,12 +953,15 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
         double x0 = xv[buf][0][gr], x1 = xv[buf][1][gr], x2 = xv[buf][2][gr];
         double v0 = xv[buf][3][gr], v1 = xv[buf][4][gr], v2 = xv[buf][5][gr];
         push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
-        x[j] = x0;
-        x[stride + j] = x1;
-        x[2 * stride + j] = x2;
-        v[j] = v0;
-        v[stride + j] = v1;
-        v[2 * stride + j] = v2;
+        double* const xo = P.xo ? P.xo : x;
+        double* const vo = P.vo ? P.vo : v;
+        xo[j] = x0;
+        xo[stride + j] = x1;
+        xo[2 * stride + j] = x2;
+        vo[j] = v0;
+        vo[stride + j] = v1;
+        vo[2 * stride + j] = v2;
+        if (P.ido) P.ido[j] = id[sj];
       }
     }
     __syncwarp();  // psi rows and xv[buf] are rewritten for the next m-tile
@@ -1165,6 +1186,7 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
   c.bcol = c.bz = -1;
   slab_cursor_load<C::NSZ>(c, lo, g, Sc);
   pf = c;
+  auto pp = c;  // perm prefetch cursor (fused sort)
   auto advance = [&](SlabCursor& it, int q, bool release) {
     while (it.k < nitems && q >= it.base + it.m) {
       if (release) {
@@ -1177,15 +1199,27 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
     }
     return it.k < nitems;
   };
-  auto prefetch = [&](int buf, int q) {
+  // fused sort: the source index of this lane's particle (p = lane & 7) of an
+  // m-tile, loaded one prefetch ahead (cursor pp) so that its latency does not
+  // stall the cp.async issue
+  auto perm_of = [&](int q) -> int {
+    int r = 0;
+    if (P.perm && advance(pp, q, false)) {
+      const int64_t b = pp.start + 8 * (int64_t)(q - pp.base) + (lane & 7);
+      if (b < pp.end) r = P.perm[b];
+    }
+    return r;
+  };
+  auto prefetch = [&](int buf, int q, int ps) {
     if (advance(pf, q, false)) {
       const int64_t b = pf.start + 8 * (int64_t)(q - pf.base);
       const int cnt = (int)min((int64_t)8, pf.end - b);
       for (int u = lane; u < 48; u += 32) {
         const int comp = u >> 3, p = u & 7;
         if (p < cnt) {
-          if (comp < 3) cp_async8(&xv[buf][comp][p], x + comp * stride + b + p);
-          else if (v) cp_async8(&xv[buf][comp][p], v + (comp - 3) * stride + b + p);
+          const int64_t sj = P.perm ? (int64_t)ps : b + p;
+          if (comp < 3) cp_async8(&xv[buf][comp][p], x + comp * stride + sj);
+          else if (v) cp_async8(&xv[buf][comp][p], v + (comp - 3) * stride + sj);
         }
       }
     }
@@ -1238,11 +1272,13 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
   };
 
   int buf = 0;
-  prefetch(0, wid);
+  prefetch(0, wid, perm_of(wid));
+  int pn = perm_of(wid + C::NW);
   for (int q = wid; advance(c, q, true); q += C::NW, buf ^= 1) {
     const int64_t b = c.start + 8 * (int64_t)(q - c.base);
     const int cnt = (int)min((int64_t)8, c.end - b);
-    prefetch(buf ^ 1, q + C::NW);
+    prefetch(buf ^ 1, q + C::NW, pn);
+    pn = perm_of(q + 2 * C::NW);
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
     stage(buf, cnt);
@@ -1307,9 +1343,9 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
       e2 += __shfl_xor_sync(0xffffffffu, e2, o);
     }
     if (tq == 0 && gr < cnt) {
-      const int64_t j = b + gr;
+      const int64_t j = b + gr, sj = src_of(P.perm, j);
       if (Eout) {
-        const int64_t k = id[j];
+        const int64_t k = id[sj];
         Eout[k] = e0;
         Eout[stride + k] = e1;
         Eout[2 * stride + k] = e2;
@@ -1318,12 +1354,15 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
         double x0 = xv[buf][0][gr], x1 = xv[buf][1][gr], x2 = xv[buf][2][gr];
         double v0 = xv[buf][3][gr], v1 = xv[buf][4][gr], v2 = xv[buf][5][gr];
         push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
-        x[j] = x0;
-        x[stride + j] = x1;
-        x[2 * stride + j] = x2;
-        v[j] = v0;
-        v[stride + j] = v1;
-        v[2 * stride + j] = v2;
+        double* const xo = P.xo ? P.xo : x;
+        double* const vo = P.vo ? P.vo : v;
+        xo[j] = x0;
+        xo[stride + j] = x1;
+        xo[2 * stride + j] = x2;
+        vo[j] = v0;
+        vo[stride + j] = v1;
+        vo[2 * stride + j] = v2;
+        if (P.ido) P.ido[j] = id[sj];
       }
     }
     __syncwarp();
@@ -1332,7 +1371,8 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
 }
 
 template <int A, int B, int Cz, bool SUB = false>
-static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, const double* s,
+static cudaError_t spread_launch(unsigned nbr, const double* x, const int* perm, int64_t stride,
+                                 const double* s,
                                  double s_uniform, const Sched& offsets, const Brick& g,
                                  const Horner& hc, double* grid, cudaStream_t st) {
   const int T = 32 * SpreadCfg<A, B, Cz>::NW;
@@ -1362,9 +1402,9 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
   cudaError_t e0 = cudaMemsetAsync(offsets.ctr, 0, sizeof(int), st);
   if (e0 != cudaSuccess) return e0;
   if (s)
-    k_spread<A, B, Cz, true, SUB><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread<A, B, Cz, true, SUB><<<nbr, T, smem, st>>>(x, perm, stride, s, s_uniform, offsets, g, hc, grid);
   else
-    k_spread<A, B, Cz, false, SUB><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread<A, B, Cz, false, SUB><<<nbr, T, smem, st>>>(x, perm, stride, s, s_uniform, offsets, g, hc, grid);
   return cudaGetLastError();
 }
 
@@ -1372,7 +1412,8 @@ static cudaError_t spread_launch(unsigned nbr, const double* x, int64_t stride, 
 #define PIF_SPREAD_WARP 1
 #endif
 template <int A, int B, int Cz, typename HC>
-static cudaError_t spread_warp_launch(unsigned nitems, const double* x, int64_t stride, const double* s,
+static cudaError_t spread_warp_launch(unsigned nitems, const double* x, const int* perm, int64_t stride,
+                                      const double* s,
                                       double s_uniform, const Sched& offsets, const Brick& g,
                                       const HC& hc, double* grid, cudaStream_t st) {
   using C = SpreadWCfg<A, B, Cz>;
@@ -1400,41 +1441,41 @@ static cudaError_t spread_warp_launch(unsigned nitems, const double* x, int64_t 
   cudaError_t e0 = cudaMemsetAsync(offsets.ctr, 0, sizeof(int), st);
   if (e0 != cudaSuccess) return e0;
   if (s)
-    k_spread_warp<A, B, Cz, true, HC><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread_warp<A, B, Cz, true, HC><<<nbr, T, smem, st>>>(x, perm, stride, s, s_uniform, offsets, g, hc, grid);
   else
-    k_spread_warp<A, B, Cz, false, HC><<<nbr, T, smem, st>>>(x, stride, s, s_uniform, offsets, g, hc, grid);
+    k_spread_warp<A, B, Cz, false, HC><<<nbr, T, smem, st>>>(x, perm, stride, s, s_uniform, offsets, g, hc, grid);
   return cudaGetLastError();
 }
 
 #ifndef PIF_SPREAD_F32PSI
 #define PIF_SPREAD_F32PSI 1
 #endif
-cudaError_t launch_spread(const double* x, int64_t stride, const double* s, double s_uniform,
-                          const Sched& offsets, const Brick& g, const Horner& hc, const HornerF* hcf,
-                          double* grid, cudaStream_t st) {
+cudaError_t launch_spread(const double* x, const int* perm, int64_t stride, const double* s,
+                          double s_uniform, const Sched& offsets, const Brick& g, const Horner& hc,
+                          const HornerF* hcf, double* grid, cudaStream_t st) {
   const unsigned ni = (unsigned)offsets.max_i;
   if (PIF_SPREAD_WARP && g.C > 1 && g.RI[0] == 10 && g.RI[1] == 10 && g.RI[2] == 8)
     return (PIF_SPREAD_F32PSI && hcf)
-               ? spread_warp_launch<10, 10, 8>(ni, x, stride, s, s_uniform, offsets, g, *hcf, grid, st)
-               : spread_warp_launch<10, 10, 8>(ni, x, stride, s, s_uniform, offsets, g, hc, grid, st);
+               ? spread_warp_launch<10, 10, 8>(ni, x, perm, stride, s, s_uniform, offsets, g, *hcf, grid, st)
+               : spread_warp_launch<10, 10, 8>(ni, x, perm, stride, s, s_uniform, offsets, g, hc, grid, st);
   if (PIF_SPREAD_WARP && g.C > 1 && g.RI[0] == 6 && g.RI[1] == 6 && g.RI[2] == 8)
     return (PIF_SPREAD_F32PSI && hcf)
-               ? spread_warp_launch<6, 6, 8>(ni, x, stride, s, s_uniform, offsets, g, *hcf, grid, st)
-               : spread_warp_launch<6, 6, 8>(ni, x, stride, s, s_uniform, offsets, g, hc, grid, st);
+               ? spread_warp_launch<6, 6, 8>(ni, x, perm, stride, s, s_uniform, offsets, g, *hcf, grid, st)
+               : spread_warp_launch<6, 6, 8>(ni, x, perm, stride, s, s_uniform, offsets, g, hc, grid, st);
   // dense w = 8 / w = 5 plans (>= 12 / 8 particles per cell, cell keys): spread
   // over the interpolation sub-bricks with the interpolation tile (10x10x8 /
   // 6x6x8 instead of 16x16x8 / 8^3: 2.6x / 1.8x fewer padded FMAs), the extra
   // REDG flush per particle being small at that density
   if (g.C > 1 && g.RI[0] == 10 && g.RI[1] == 10 && g.RI[2] == 8)
-    return spread_launch<10, 10, 8, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
+    return spread_launch<10, 10, 8, true>((unsigned)offsets.max_i, x, perm, stride, s, s_uniform, offsets,
                                           g, hc, grid, st);
   if (g.C > 1 && g.RI[0] == 6 && g.RI[1] == 6 && g.RI[2] == 8)
-    return spread_launch<6, 6, 8, true>((unsigned)offsets.max_i, x, stride, s, s_uniform, offsets,
+    return spread_launch<6, 6, 8, true>((unsigned)offsets.max_i, x, perm, stride, s, s_uniform, offsets,
                                         g, hc, grid, st);
   const unsigned nbr = (unsigned)offsets.max_s;  // upper bound on spread items
 #define PIF_SPREAD(A, B, Cz)                                        \
   if (g.RS[0] == A && g.RS[1] == B && g.RS[2] == Cz)                \
-    return spread_launch<A, B, Cz>(nbr, x, stride, s, s_uniform, offsets, g, hc, grid, st);
+    return spread_launch<A, B, Cz>(nbr, x, perm, stride, s, s_uniform, offsets, g, hc, grid, st);
   PIF_SPREAD(8, 8, 8)
   PIF_SPREAD(12, 12, 12)
   PIF_SPREAD(16, 16, 16)
