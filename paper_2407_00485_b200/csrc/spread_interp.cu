@@ -301,7 +301,7 @@ struct SpreadCfg {
   // resident CTAs per SM the register budget must allow: small tiles (5 warps)
   // fit 5 by shared memory, and the register allocation decides between 3 and 4
   static constexpr int MINB = NW <= 5 ? 4 : PIF_SPREAD_MINB;
-  static_assert((RX + RY + spread_pad_rows(RX, RY) + (RZ + 7) / 8 * 8) * (kChunk + 4) >= RX * RY * RZ,
+  static_assert(!BULK || (RX + RY + spread_pad_rows(RX, RY) + (RZ + 7) / 8 * 8) * (kChunk + 4) >= RX * RY * RZ,
                 "the bulk-flush tile reuses the psi rows");
   static_assert(NCT % CT == 0, "tile shape");
 };
