@@ -526,6 +526,20 @@ def test_fp32_type2_vs_nudft(tol, npart):
     assert err > 1e-9  # it really ran in single precision
 
 
+@pytest.mark.parametrize("tol", [1e-3, 1e-4, 1e-5])  # w = 4, 5, 6
+@pytest.mark.parametrize("npart", [16384, 16 * 16 ** 3 + 3])  # sparse / dense tiles
+def test_fp32_type1_vs_nudft(tol, npart):
+    """PIF_FLAG_FP32 type-1 (the spread accumulates in fp64; on the dense
+    warp-owned tiles its ES weights come from the fp32 Horner chains) within
+    10 eps of the exact NUDFT, signed strengths, ragged count."""
+    phys = landau_physics()
+    x, _ = landau_state(npart, 54)
+    s = np.random.default_rng(55).standard_normal(npart)
+    sim = sim_for(phys, P.propagator("pif", 8, 0.05, tol=tol, fp32=True), n=npart)
+    got = P.pif_debug_type1(sim.ctx, 0, x, s, 8)
+    assert rel_l2(got, O.nudft_type1(x, s, 8, phys.L)) <= 10 * tol
+
+
 def test_fp32_coarse_steps_vs_oracle():
     """5 steps of the fp32 coarse propagator (eps_g = 1e-4, dense w = 5 tile) vs
     the exact oracle, with the bound of test_dense_tiles_steps_vs_oracle
