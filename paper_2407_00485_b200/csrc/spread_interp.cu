@@ -90,9 +90,6 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
 __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-#ifndef PIF_MBAR_LIGHT
-#define PIF_MBAR_LIGHT 1
-#endif
 // Wait for completion of the phase with the given parity.  Bounded: a protocol
 // error traps (kernel error) after ~10 s instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
@@ -105,17 +102,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
         : "r"(smem_u32(b)), "r"(parity)
         : "memory");
     if (done) return;
-#if PIF_MBAR_LIGHT
     // the clock is read once per 256 polls (a spinning warp shares its SMSP's
     // issue slots with the MMA warps)
     if ((spin & 255) == 0) {
       if (spin == 0) t0 = clock64();
       else if (clock64() - t0 > 20000000000LL) __trap();
     }
-#else
-    if (spin == 0) t0 = clock64();
-    else if (clock64() - t0 > 20000000000LL) __trap();
-#endif
   }
 }
 
@@ -1003,9 +995,6 @@ __global__ void __launch_bounds__(32 * (InterpCfg<RX, RY, RZ>::NW + InterpCfg<RX
 // Slab layout: [cy * CS + cx][d][r] (r < SBZ rows), CS = 18 for BX = 16: the
 // B-fragment reads (lane (g, t): tile row 8 nt + g, sub-window column 4 ks + t)
 // are conflict-free for every sub-brick offset (checked exhaustively).
-#ifndef PIF_KLOOP_INC
-#define PIF_KLOOP_INC 1
-#endif
 template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX, int ZR>
 struct SlabCfg {
   using I = InterpCfg<RX, RY, RZ>;
@@ -1318,7 +1307,6 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
     const double* pxr = wpsi + gr * C::SX;
     const double* pyr = wpsi + C::OY + gr * C::SY;
     int cx = tq, cy = 0;  // column 4 ks + tq of the window (RXm >= 4)
-#if PIF_KLOOP_INC
     // B offset (cy CS + cx) 3 SBZ kept incrementally: + 4 columns per k step,
     // + (CS - RXm) columns at a window-row wrap.  Used for the 1-row slabs
     // (w = 8: C5 fine interp 14.15 -> 14.02 ms); the 4-row slabs (w = 13)
@@ -1343,9 +1331,7 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
 #pragma unroll
         for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, Pb[nt][o + d * SBZ]);
     }
-    } else
-#endif
-    {
+    } else {
 #pragma unroll 2
     for (int ks = 0; ks < KSm - 1; ++ks) {
       const double a = pxr[cx] * pyr[cy];
