@@ -230,7 +230,10 @@ pif_status pif_comm_info(pif_ctx ctx, int32_t* world_nranks, int32_t* space_nran
    reset -- phase_ms[PIF_NPHASES] in the order sort, spread, fft_fwd, box
    (deconvolve/truncate), allreduce, poisson (+pad), fft_inv, interp_push,
    pic_deposit, pic_gather_push, other -- and the number of the library's own
-   kernels launched (cuFFT / NCCL kernels not counted).  reset != 0 clears both. */
+   kernels launched (cuFFT / NCCL kernels not counted).  In a step that pushes,
+   "sort" is the bin count, schedule and permutation only: the reorder itself
+   happens inside the spread (permuted reads) and interp_push (permuted reads,
+   sorted writes).  reset != 0 clears both. */
 #define PIF_NPHASES 11
 pif_status pif_profile(pif_ctx ctx, int enable);
 pif_status pif_profile_read(pif_ctx ctx, double* phase_ms, int32_t n_phases, int64_t* launches,
