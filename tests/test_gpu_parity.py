@@ -155,6 +155,37 @@ def test_fine_steps_vs_oracle(case, N, npart, dt):
     assert ce <= 1e-10
 
 
+@pytest.mark.parametrize("tol", [1e-12, 1e-7])  # brick / dense warp-owned + 1-row slab tiles
+def test_steps_interleaved_with_diagnostics_vs_oracle(tol):
+    """Steps with a diagnostic after each one: the field-only solve of
+    field_energy (no push: the gather sort) alternates with pushing steps (sort
+    fused into spread and interp+push); the state after 8 steps and
+    every W match the exact oracle (tolerance 10 eps on the field-driven
+    change, as test_dense_tiles_steps_vs_oracle)."""
+    phys = landau_physics()
+    n, N, dt, K = 16 * 16 ** 3 + 5, 8, 0.05, 8
+    x0, v0 = landau_state(n, 71)
+    sim = sim_for(phys, P.propagator("pif", N, dt, tol=tol), n=n)
+    sim.set_state(torch.from_numpy(x0).cuda(), torch.from_numpy(v0).cuda())
+    ph = O.PhysicsParams.from_inputs(phys)
+    prop = O.Propagator("pif", N, dt)
+    xr, vr = x0, v0
+    for _ in range(K):
+        sim.step(1)
+        W, ke, _, _ = sim.field_energy()
+        xr, vr = O.run(xr, vr, 1, prop, ph)
+        Wr, ker, _, _ = O.diagnostics(xr, vr, prop, ph)
+        # (floor 1e-10: the bound of test_fine_steps_vs_oracle at eps = 1e-12)
+        assert np.all(np.abs(W - Wr) <= max(10 * tol, 1e-10) * Wr.sum())
+        assert abs(ke - ker) <= max(10 * tol, 1e-10) * ker
+    x, v = sim.get_state()
+    x, v = x.cpu().numpy(), v.cpu().numpy()
+    assert np.linalg.norm(v - vr) <= 10 * tol * np.linalg.norm(vr - v0) + 1e-10 * np.linalg.norm(vr)
+    disp_ref = O.min_image(xr - (x0 + K * dt * v0), phys.L)
+    assert np.linalg.norm(O.min_image(x - xr, phys.L)) <= (10 * tol * np.linalg.norm(disp_ref)
+                                                           + 1e-10 * phys.L * math.sqrt(n))
+
+
 def test_momentum_conservation_any_tolerance():
     """Momentum drift <= 1e-13 sum m|v| for eps = 1e-4."""
     phys = landau_physics()
