@@ -1019,8 +1019,20 @@ struct SlabCfg {
 #ifndef PIF_SLAB_NW
 #define PIF_SLAB_NW 16
 #endif
+#ifndef PIF_SLAB_MT2
+#define PIF_SLAB_MT2 1
+#endif
+  // m-unit: MT m-tiles of 8 particles contracted together over ONE window (the
+  // union of their cells), sharing every B fragment load and the per-unit
+  // cursor / prefetch / window work.  MT = 2 for the 1-row slabs (w = 8: 16 k
+  // steps x 3 DMMAs per m-tile, so the per-m-tile work dominated), else 1.
+  static constexpr int MT = (SBZ == 1 && PIF_SLAB_MT2) ? 2 : 1;
+  static constexpr int MP = 8 * MT;                 // particles per m-unit
+  static constexpr int OYM = MP * SX + 1, OZM = OYM + MP * SY + 1;
+  static constexpr int WPM = OZM + MP * SZ;         // psi doubles per warp
+  static_assert(OZM % 2 == 0 && WPM % 2 == 0, "pz rows are read as double2");
   static constexpr int BYTES = 232448 - 2 * ND * 8 - 64;
-  static constexpr int NWFIT = (BYTES / 8 - NS * SLAB) / (WP + 96);
+  static constexpr int NWFIT = (BYTES / 8 - NS * SLAB) / (WPM + 12 * MP);
 #ifndef PIF_SLAB_NW1
 #define PIF_SLAB_NW1 20  // one-row slabs (w = 8 dense: smaller psi rows; 20 measured 2.4 % faster
                          // than 24 and 6 % faster than 16 after the fused sort, C5 fine interp)
@@ -1042,8 +1054,8 @@ template <int RX, int RY, int RZ, int BX, int BY, int SBZ, int CSX, int ZR>
 struct SlabSmem {
   using C = SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR>;
   double slab[C::NS][C::SLAB];
-  double psi[C::NW][C::WP];
-  double xv[C::NW][2][6][8];
+  double psi[C::NW][C::WPM];
+  double xv[C::NW][2][6][C::MP];
   unsigned long long full[C::ND], done[C::ND];
   int range[2];
 };
@@ -1059,14 +1071,14 @@ struct SlabCursor {
   int bcol, bz;  // brick column (bx * NB1 + by) and bz of item k
 };
 
-template <int NSZ>
+template <int NSZ, int MP = 8>
 __device__ __forceinline__ void slab_cursor_load(SlabCursor& it, int lo, const Brick& g,
                                                  const Sched& Sc) {
   const int4 e = Sc.iitems[lo + it.k];
   const int4 f = Sc.iinfo[lo + it.k];  // {bx, by, bz, sx | sy << 16}
   it.start = e.y;
   it.end = e.z;
-  it.m = (int)((e.z - e.y + 7) >> 3);
+  it.m = (int)((e.z - e.y + MP - 1) / MP);
   const int bx = f.x, by = f.y, bz = f.z, sx = f.w & 0xffff, sy = f.w >> 16;
   const int bcol = bx * g.NB[1] + by;
   it.ox = sx * g.ib[0];
@@ -1181,7 +1193,8 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
   // ---- consumers (as k_interp_push; B fragments from the slab ring)
   const int gr = lane >> 2, tq = lane & 3;
   double* const wpsi = S.psi[wid];
-  double (*const xv)[6][8] = S.xv[wid];
+  double (*const xv)[6][C::MP] = S.xv[wid];
+  constexpr int MT = C::MT, MP = C::MP;
   const double two_over_w = 2.0 / g.w;
   const double flo = g.odd ? -0.5 : 0.0;
   SlabCursor c, pf;
@@ -1189,7 +1202,7 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
   c.base = pf.base = 0;
   c.V = 0;
   c.bcol = c.bz = -1;
-  slab_cursor_load<C::NSZ>(c, lo, g, Sc);
+  slab_cursor_load<C::NSZ, MP>(c, lo, g, Sc);
   pf = c;
   auto pp = c;  // perm prefetch cursor (fused sort)
   auto advance = [&](SlabCursor& it, int q, bool release) {
@@ -1200,7 +1213,7 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
         if (lane == 0) mbar_arrive(&S.done[it.k % C::ND]);
       }
       it.base += it.m;
-      if (++it.k < nitems) slab_cursor_load<C::NSZ>(it, lo, g, Sc);
+      if (++it.k < nitems) slab_cursor_load<C::NSZ, MP>(it, lo, g, Sc);
     }
     return it.k < nitems;
   };
@@ -1210,17 +1223,17 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
   auto perm_of = [&](int q) -> int {
     int r = 0;
     if (P.perm && advance(pp, q, false)) {
-      const int64_t b = pp.start + 8 * (int64_t)(q - pp.base) + (lane & 7);
+      const int64_t b = pp.start + MP * (int64_t)(q - pp.base) + (lane % MP);
       if (b < pp.end) r = P.perm[b];
     }
     return r;
   };
   auto prefetch = [&](int buf, int q, int ps) {
     if (advance(pf, q, false)) {
-      const int64_t b = pf.start + 8 * (int64_t)(q - pf.base);
-      const int cnt = (int)min((int64_t)8, pf.end - b);
-      for (int u = lane; u < 48; u += 32) {
-        const int comp = u >> 3, p = u & 7;
+      const int64_t b = pf.start + MP * (int64_t)(q - pf.base);
+      const int cnt = (int)min((int64_t)MP, pf.end - b);
+      for (int u = lane; u < 6 * MP; u += 32) {
+        const int comp = u / MP, p = u % MP;
         if (p < cnt) {
           const int64_t sj = P.perm ? (int64_t)ps : b + p;
           if (comp < 3) cp_async8(&xv[buf][comp][p], x + comp * stride + sj);
@@ -1236,19 +1249,29 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
   // from column (ox_m, oy_m) of the sub-brick tile -- 13 x 13 when all 8 share a
   // cell.  Rows are zero outside the window up to C::FILL entries.
   int ox_m = 0, oy_m = 0, ex_x = 0, ex_y = 0;
+  // (m-unit of MT m-tiles: lane = (particle p of m-tile r, dimension d), the
+  // window is the union over the unit's MP particles)
   auto stage = [&](int buf, int cnt) {
     const int p = lane & 7, d = lane >> 3;
-    const bool valid = lane < 24 && p < cnt;
-    int rel = 0;
-    double f = 0.0;
-    if (valid) {
-      const int T0d = d == 0 ? c.T0[0] : (d == 1 ? c.T0[1] : c.T0[2]);
-      double xs = xv[buf][d][p] * g.scale;
-      const int a = anchor_of(xs, g);
-      f = xs - (double)a;
-      rel = a - g.hw - T0d;
+    const int T0d = d == 0 ? c.T0[0] : (d == 1 ? c.T0[1] : c.T0[2]);
+    bool valid[MT];
+    int rel[MT];
+    double f[MT];
+    int mn = 1 << 20, mx = -1;
+#pragma unroll
+    for (int r = 0; r < MT; ++r) {
+      valid[r] = lane < 24 && 8 * r + p < cnt;
+      rel[r] = 0;
+      f[r] = 0.0;
+      if (valid[r]) {
+        double xs = xv[buf][d][8 * r + p] * g.scale;
+        const int a = anchor_of(xs, g);
+        f[r] = xs - (double)a;
+        rel[r] = a - g.hw - T0d;
+        mn = min(mn, rel[r]);
+        mx = max(mx, rel[r]);
+      }
     }
-    int mn = valid ? rel : (1 << 20), mx = valid ? rel : -1;
 #pragma unroll
     for (int o = 1; o <= 4; o <<= 1) {
       mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -1261,18 +1284,23 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
     // zero fill, then the weights.  One-row slabs (w = 8): the warp's psi rows
     // with contiguous 16-byte stores (C5 fine interp 12.67 -> 12.41 ms); w = 13:
     // per staging lane and row (the cooperative fill measured 0.5 % slower)
-    double* row = wpsi + (d == 0 ? p * C::SX : (d == 1 ? C::OY + p * C::SY : C::OZ + p * C::SZ));
     if constexpr (SBZ == 1) {
 #pragma unroll
-      for (int i = lane; i < C::WP / 2; i += 32) reinterpret_cast<double2*>(wpsi)[i] = make_double2(0.0, 0.0);
+      for (int i = lane; i < C::WPM / 2; i += 32) reinterpret_cast<double2*>(wpsi)[i] = make_double2(0.0, 0.0);
       __syncwarp();
-    } else if (lane < 24) {
-#pragma unroll
-      for (int u = 0; u < C::FILL; ++u) row[u] = 0.0;
     }
-    if (valid) {
-      const double sv = 2.0 * (f - flo) - 1.0;
-      psi_row(row + rel - (d == 0 ? ox_m : (d == 1 ? oy_m : 0)), 0, f, sv, hc, g, two_over_w);
+#pragma unroll
+    for (int r = 0; r < MT; ++r) {
+      const int pr = 8 * r + p;
+      double* row = wpsi + (d == 0 ? pr * C::SX : (d == 1 ? C::OYM + pr * C::SY : C::OZM + pr * C::SZ));
+      if (SBZ != 1 && lane < 24) {
+#pragma unroll
+        for (int u = 0; u < C::FILL; ++u) row[u] = 0.0;
+      }
+      if (valid[r]) {
+        const double sv = 2.0 * (f[r] - flo) - 1.0;
+        psi_row(row + rel[r] - (d == 0 ? ox_m : (d == 1 ? oy_m : 0)), 0, f[r], sv, hc, g, two_over_w);
+      }
     }
   };
 
@@ -1280,8 +1308,8 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
   prefetch(0, wid, perm_of(wid));
   int pn = perm_of(wid + C::NW);
   for (int q = wid; advance(c, q, true); q += C::NW, buf ^= 1) {
-    const int64_t b = c.start + 8 * (int64_t)(q - c.base);
-    const int cnt = (int)min((int64_t)8, c.end - b);
+    const int64_t b = c.start + MP * (int64_t)(q - c.base);
+    const int cnt = (int)min((int64_t)MP, c.end - b);
     prefetch(buf ^ 1, q + C::NW, pn);
     pn = perm_of(q + 2 * C::NW);
     asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -1299,13 +1327,20 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
     }
     const int RXm = g.w + ex_x, RYm = g.w + ex_y;  // m-tile window (<= RX x RY)
     const int KSm = (RXm * RYm + 3) >> 2;
-    double acc[C::NT][3][2];
+    double acc[MT][C::NT][3][2];
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt)
+    for (int r = 0; r < MT; ++r)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) acc[nt][d][0] = acc[nt][d][1] = 0.0;
-    const double* pxr = wpsi + gr * C::SX;
-    const double* pyr = wpsi + C::OY + gr * C::SY;
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) acc[r][nt][d][0] = acc[r][nt][d][1] = 0.0;
+    const double* pxr[MT];
+    const double* pyr[MT];
+#pragma unroll
+    for (int r = 0; r < MT; ++r) {
+      pxr[r] = wpsi + (8 * r + gr) * C::SX;
+      pyr[r] = wpsi + C::OYM + (8 * r + gr) * C::SY;
+    }
     int cx = tq, cy = 0;  // column 4 ks + tq of the window (RXm >= 4)
     // B offset (cy CS + cx) 3 SBZ kept incrementally: + 4 columns per k step,
     // + (CS - RXm) columns at a window-row wrap.  Used for the 1-row slabs
@@ -1317,7 +1352,9 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
     const int wrap_off = (C::CS - RXm) * 3 * SBZ;
 #pragma unroll 2
     for (int ks = 0; ks < KSm - 1; ++ks) {
-      const double a = pxr[cx] * pyr[cy];
+      double a[MT];
+#pragma unroll
+      for (int r = 0; r < MT; ++r) a[r] = pxr[r][cx] * pyr[r][cy];
       const int o = off;
       cx += 4;
       off += 4 * 3 * SBZ;
@@ -1329,12 +1366,18 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, Pb[nt][o + d * SBZ]);
+        for (int d = 0; d < 3; ++d) {
+          const double bb = Pb[nt][o + d * SBZ];
+#pragma unroll
+          for (int r = 0; r < MT; ++r) dmma(acc[r][nt][d], a[r], bb);
+        }
     }
     } else {
 #pragma unroll 2
     for (int ks = 0; ks < KSm - 1; ++ks) {
-      const double a = pxr[cx] * pyr[cy];
+      double a[MT];
+#pragma unroll
+      for (int r = 0; r < MT; ++r) a[r] = pxr[r][cx] * pyr[r][cy];
       const int off = (cy * C::CS + cx) * 3 * SBZ;
       cx += 4;
       if (cx >= RXm) {
@@ -1344,37 +1387,59 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, Pb[nt][off + d * SBZ]);
+        for (int d = 0; d < 3; ++d) {
+          const double bb = Pb[nt][off + d * SBZ];
+#pragma unroll
+          for (int r = 0; r < MT; ++r) dmma(acc[r][nt][d], a[r], bb);
+        }
     }
     }
     {
       // last k step: columns past the window (cy == RYm) have A = 0 (py rows are
       // zero-filled past the window) and read B from the window's last row, so
       // every B operand is landed data of this item's slabs (no read outside them)
-      const double a = pxr[cx] * pyr[cy];
+      double a[MT];
+#pragma unroll
+      for (int r = 0; r < MT; ++r) a[r] = pxr[r][cx] * pyr[r][cy];
       const int off = ((cy < RYm ? cy : RYm - 1) * C::CS + cx) * 3 * SBZ;
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) dmma(acc[nt][d], a, Pb[nt][off + d * SBZ]);
+        for (int d = 0; d < 3; ++d) {
+          const double bb = Pb[nt][off + d * SBZ];
+#pragma unroll
+          for (int r = 0; r < MT; ++r) dmma(acc[r][nt][d], a[r], bb);
+        }
     }
+    // lanes tq = r hold (after the xor reduction every tq lane does) the field
+    // of particle 8 r + gr; lane tq = r < MT pushes it
     double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-    const double* pzr = wpsi + C::OZ + gr * C::SZ;
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt) {
-      const double2 wz = *reinterpret_cast<const double2*>(pzr + 8 * nt + 2 * tq);
-      e0 = fma(wz.x, acc[nt][0][0], fma(wz.y, acc[nt][0][1], e0));
-      e1 = fma(wz.x, acc[nt][1][0], fma(wz.y, acc[nt][1][1], e1));
-      e2 = fma(wz.x, acc[nt][2][0], fma(wz.y, acc[nt][2][1], e2));
-    }
+    for (int r = 0; r < MT; ++r) {
+      double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+      const double* pzr = wpsi + C::OZM + (8 * r + gr) * C::SZ;
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-      e0 += __shfl_xor_sync(0xffffffffu, e0, o);
-      e1 += __shfl_xor_sync(0xffffffffu, e1, o);
-      e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+      for (int nt = 0; nt < C::NT; ++nt) {
+        const double2 wz = *reinterpret_cast<const double2*>(pzr + 8 * nt + 2 * tq);
+        f0 = fma(wz.x, acc[r][nt][0][0], fma(wz.y, acc[r][nt][0][1], f0));
+        f1 = fma(wz.x, acc[r][nt][1][0], fma(wz.y, acc[r][nt][1][1], f1));
+        f2 = fma(wz.x, acc[r][nt][2][0], fma(wz.y, acc[r][nt][2][1], f2));
+      }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        f0 += __shfl_xor_sync(0xffffffffu, f0, o);
+        f1 += __shfl_xor_sync(0xffffffffu, f1, o);
+        f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+      }
+      if (tq == r) {
+        e0 = f0;
+        e1 = f1;
+        e2 = f2;
+      }
     }
-    if (tq == 0 && gr < cnt) {
-      const int64_t j = b + gr, sj = src_of(P.perm, j);
+    const int pq = 8 * tq + gr;  // this lane's particle in the m-unit (tq < MT)
+    if (tq < MT && pq < cnt) {
+      const int64_t j = b + pq, sj = src_of(P.perm, j);
       if (Eout) {
         const int64_t k = id[sj];
         Eout[k] = e0;
@@ -1382,8 +1447,8 @@ __global__ void __launch_bounds__(32 * (SlabCfg<RX, RY, RZ, BX, BY, SBZ, CSX, ZR
         Eout[2 * stride + k] = e2;
       }
       if (P.kicks > 0 || P.drift) {
-        double x0 = xv[buf][0][gr], x1 = xv[buf][1][gr], x2 = xv[buf][2][gr];
-        double v0 = xv[buf][3][gr], v1 = xv[buf][4][gr], v2 = xv[buf][5][gr];
+        double x0 = xv[buf][0][pq], x1 = xv[buf][1][pq], x2 = xv[buf][2][pq];
+        double v0 = xv[buf][3][pq], v1 = xv[buf][4][pq], v2 = xv[buf][5][pq];
         push_particle(x0, x1, x2, v0, v1, v2, e0, e1, e2, P);
         double* const xo = P.xo ? P.xo : x;
         double* const vo = P.vo ? P.vo : v;
