@@ -1034,8 +1034,9 @@ struct SlabCfg {
   static constexpr int BYTES = 232448 - 2 * ND * 8 - 64;
   static constexpr int NWFIT = (BYTES / 8 - NS * SLAB) / (WPM + 12 * MP);
 #ifndef PIF_SLAB_NW1
-#define PIF_SLAB_NW1 20  // one-row slabs (w = 8 dense: smaller psi rows; 20 measured 2.4 % faster
-                         // than 24 and 6 % faster than 16 after the fused sort, C5 fine interp)
+#define PIF_SLAB_NW1 16  // one-row slabs (w = 8 dense) with 16-particle m-units: 16 measured
+                         // 1.3 % faster than 18 (the shared-memory fit) and 6 % faster than 14
+                         // (with 8-particle m-tiles 20 was best, 2.4 % ahead of 24)
 #endif
   static constexpr int NWCAP = SBZ == 1 ? PIF_SLAB_NW1 : PIF_SLAB_NW;
   static constexpr int NW = NWFIT < NWCAP ? NWFIT : NWCAP;
